@@ -1,0 +1,233 @@
+/*
+ * countmc_b200.h — C-ABI drop-in boundary for the B200-native Gibbs sweep.
+ *
+ * This is the boundary a host program links against in place of the
+ * reference `countmc::GibbsEngine` (reference: proj/include/countmc/engine.hpp:110-159,
+ * implementation proj/src/engine.cpp:42-483).  Plain pointers and sizes
+ * only; no C++ or torch types cross it.  Every entry point returns an int
+ * status (CMC_OK == 0) and, where it can fail, fills a cmc_error.
+ *
+ * Packed array layouts (doubles, reference AoS order, so a caller can copy
+ * the reference structs in and out with plain memcpy):
+ *
+ *   state  (S = G*N + G + G*L + 2*L + 2):   [eps G x N | gamma G | beta G x L |
+ *                                            theta L | sigma L | nu | tau]
+ *       reference ChainState, proj/include/countmc/types.hpp:86-108
+ *   tuning (T = G*N + G + G*L + L + 2), one array for SliceVar::w and one for
+ *       SliceVar::w_aux:                    [eps G x N | gamma G | beta G x L |
+ *                                            sigma L | nu | tau]
+ *       reference TuningState, proj/include/countmc/engine.hpp:58-74
+ *   accumulators (A = 2 + 2*L + G*L + G + G*N):
+ *                                           [nu | tau | theta L | sigma L |
+ *                                            beta G x L | gamma G | eps G x N]
+ *       reference ChainOutput, proj/include/countmc/engine.hpp:90-108
+ */
+#ifndef COUNTMC_B200_H
+#define COUNTMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMC_OK 0
+#define CMC_ERR_CONFIG 1 /* reference ConfigError (errors.hpp:10-13)      */
+#define CMC_ERR_STALL 2  /* reference SamplerStallError (errors.hpp:36-71) */
+#define CMC_ERR_CUDA 3   /* device/runtime failure                         */
+#define CMC_ERR_NCCL 4   /* collective failure (multi-GPU)                 */
+#define CMC_ERR_ARG 5    /* bad pointer / index at the boundary            */
+
+/* Sampler modes, reference SamplerMode (engine.hpp:19). */
+#define CMC_SLICE_FAITHFUL 0
+#define CMC_CONJUGATE_DIRECT 1
+
+/* Contrast parameter families, reference ParamFamily (streaming.hpp:45). */
+#define CMC_FAM_BETA_COL 0
+#define CMC_FAM_GAMMA 1
+#define CMC_FAM_THETA 2
+#define CMC_FAM_SIGMA 3
+#define CMC_FAM_NU 4
+#define CMC_FAM_TAU 5
+
+/* Error record.  For CMC_ERR_STALL the fields mirror SamplerStallError:
+ * step in {"epsilon","gamma","nu","tau","beta","sigma"}, 1-based
+ * (index1, index2) with -1 where not applicable, the stalled x0, width
+ * and iteration; msg is formatted exactly as errors.cpp:8-16 does. */
+typedef struct cmc_error {
+  int code;
+  char step[16];
+  long index1;
+  long index2;
+  long iteration;
+  double x0;
+  double width;
+  char msg[256];
+} cmc_error;
+
+/* Data + model.  Replaces CountMatrix (types.hpp:50-60) and ModelSpec
+ * (types.hpp:74-83).  counts is G x N row-major (the reference Grid); X is
+ * N x L row-major; priors as PriorConfig (types.hpp:62-72), c and s already
+ * resolved to length L (PriorConfig::resolve, types.cpp:38-43). */
+typedef struct cmc_problem {
+  long G;
+  long N;
+  long L;
+  const long long* counts;
+  const double* X;
+  const double* h;
+  double a;
+  double b;
+  double d;
+  const double* c;
+  const double* s;
+} cmc_problem;
+
+/* RunConfig (engine.hpp:21-36) with SliceConfig (slice.hpp:11-17) inlined.
+ * tune_cutoff < 0 resolves to min(500, burnin/10) (engine.cpp:33). */
+typedef struct cmc_run_config {
+  long chains;
+  long iterations;
+  long burnin;
+  long tune_cutoff;
+  long thin;
+  uint64_t seed;
+  int max_step_out;
+  int max_shrink;
+  double w_init;
+  long save_genes;
+  int workers;
+  int sampler_mode;
+  int concurrent_chains;
+} cmc_run_config;
+
+/* Flattened ContrastSpec list (streaming.hpp:59-66).  Contrast k owns
+ * n_terms[k] consecutive terms; term t owns n_coefs[t] consecutive
+ * (family, index, coef) triples and threshold[t].  Scope (per gene vs
+ * global) is inferred as ContrastSpec::finalize does (streaming.cpp:76-88). */
+typedef struct cmc_contrast_set {
+  int n_contrasts;
+  const int* n_terms;
+  const int* n_coefs;
+  const double* threshold;
+  const int* family;
+  const int* index;
+  const double* coef;
+} cmc_contrast_set;
+
+/* Destination buffers for one chain's ChainOutput; any pointer may be NULL.
+ * Sizes: acc_* [A]; contrast_prob [sum over contrasts of (per_gene ? G : 1)];
+ * contrast_count [n_contrasts]; samples [n_cols * n_rows] column-major
+ * (samples[col * n_rows + row], reference samples[column][row]);
+ * sample_iters [n_rows]; final_state [S]. */
+typedef struct cmc_output_view {
+  long* acc_count;
+  double* acc_mean;
+  double* acc_meansq;
+  double* acc_mean_c;
+  double* acc_meansq_c;
+  double* contrast_prob;
+  long* contrast_count;
+  double* samples;
+  long* sample_iters;
+  uint64_t* clamp_events;
+  double* final_state;
+  double* step_seconds; /* [7]; the fused sweep reports its device time in
+                           slot 0 (steps 1,2,5 are one kernel) and the hyper
+                           tail in slot 2 */
+} cmc_output_view;
+
+typedef struct cmc_engine cmc_engine;
+
+/* Library identity: returns a static string (build flags, arch). */
+const char* cmc_version(void);
+
+/* GibbsEngine::GibbsEngine (engine.cpp:42-91): validates inputs, resolves
+ * the config, precomputes A = y X and the column groups, selects saved
+ * genes, uploads the SoA problem to `device` and allocates state for all
+ * chains.  Rank/world describe gene sharding (1 GPU: rank 0 of 1). */
+int cmc_engine_create(const cmc_problem* problem, const cmc_run_config* config,
+                      const cmc_contrast_set* contrasts, int device,
+                      cmc_engine** out, cmc_error* err);
+int cmc_engine_destroy(cmc_engine* engine);
+
+/* Sizes: G, N, L, chains, number of saved genes, thinned columns, rows. */
+int cmc_engine_dims(const cmc_engine* engine, long* G, long* N, long* L,
+                    long* chains, long* n_saved, long* n_cols, long* n_rows);
+/* GibbsEngine::saved_genes (engine.hpp:117), 0-based, ascending. */
+int cmc_engine_saved_genes(const cmc_engine* engine, long* out);
+/* RunConfig after resolve(): tune_cutoff etc. */
+int cmc_engine_config(const cmc_engine* engine, cmc_run_config* out);
+
+/* GibbsEngine::initial_state (engine.cpp:98-142) into a host [S] array. */
+int cmc_engine_initial_state(const cmc_engine* engine, long chain,
+                             double* state, cmc_error* err);
+
+/* Device-resident state of one chain: upload/download the packed state
+ * and tuning (w, w_aux).  Tuning pointers may be NULL on get. */
+int cmc_engine_set_state(cmc_engine* engine, long chain, const double* state,
+                         const double* tuning_w, const double* tuning_waux,
+                         cmc_error* err);
+int cmc_engine_get_state(cmc_engine* engine, long chain, double* state,
+                         double* tuning_w, double* tuning_waux, cmc_error* err);
+
+/* GibbsEngine::iterate (engine.cpp:161-370): one full sweep at global
+ * iteration m (1-based) of the device-resident state of `chain`.  Tuning is
+ * active while m <= burnin.  clamps (may be NULL) is incremented by the
+ * number of clamp events, as ClampCounter::bump does (model.hpp:18-26). */
+int cmc_engine_iterate(cmc_engine* engine, long chain, long m,
+                       uint64_t* clamps, cmc_error* err);
+
+/* GibbsEngine::run (engine.cpp:457-483) for every chain: initial state,
+ * burn-in + monitored iterations, accumulators, contrasts, thinning.
+ * Chains are batched across the grid; the result per chain equals the
+ * reference's run_chain(c) (engine.cpp:378-455). */
+int cmc_engine_run(cmc_engine* engine, cmc_error* err);
+
+/* The same run split in pieces for benchmarking and progress reporting:
+ * begin() loads every chain's initial state and fresh tuning and clears
+ * the monitors; sweeps(m_begin, m_end) enqueues iterations
+ * m_begin..m_end-1 of run_chain's loop body for all chains on the
+ * engine's stream (asynchronous, replayed from a CUDA graph); sync()
+ * waits and turns a device stall record into CMC_ERR_STALL. */
+int cmc_engine_begin(cmc_engine* engine, cmc_error* err);
+int cmc_engine_sweeps(cmc_engine* engine, long m_begin, long m_end,
+                      cmc_error* err);
+int cmc_engine_sync(cmc_engine* engine, cmc_error* err);
+/* cudaStream_t the engine launches on (for event timing by the caller). */
+void* cmc_engine_stream(cmc_engine* engine);
+/* Kernel launches per sweep (gene kernel + hyper tail [+ contrast]). */
+int cmc_engine_launches_per_sweep(const cmc_engine* engine);
+
+/* ChainOutput of one chain after run()/sweeps(); see cmc_output_view. */
+int cmc_engine_get_output(cmc_engine* engine, long chain,
+                          const cmc_output_view* out, cmc_error* err);
+
+/* Synthetic data in the shape of simulate.cpp:28-90 (beta ~ N(theta,
+ * sigma^2), gamma ~ IG(nu/2, nu tau/2), eps ~ N(0, gamma), y ~ Poisson):
+ * host-side input generator for benchmarks/tests (not on the hot path).
+ * counts_out is G x N row-major. */
+int cmc_simulate(long G, long N, long L, const double* X, const double* h,
+                 double nu, double tau, const double* theta,
+                 const double* sigma, uint64_t seed, long long* counts_out,
+                 cmc_error* err);
+
+/* Gene sharding (multi-GPU, one process per GPU): restricts the engine to
+ * genes [g_begin, g_end) of the full problem (g_begin a multiple of 1024,
+ * the reference reduction leaf, parallel.hpp:60) and joins an NCCL clique
+ * identified by the 128-byte ncclUniqueId.  Leaf partial sums are
+ * all-gathered every sweep, so results are bit-identical for any rank
+ * count.  Must be called before begin()/iterate(). */
+int cmc_engine_shard(cmc_engine* engine, int rank, int world,
+                     const void* nccl_unique_id, cmc_error* err);
+/* Writes the 128-byte ncclUniqueId for rank 0 to broadcast. */
+int cmc_nccl_unique_id(void* out128, cmc_error* err);
+/* Shard bounds for gene count G over `world` ranks (leaf aligned). */
+int cmc_shard_bounds(long G, int rank, int world, long* g_begin, long* g_end);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COUNTMC_B200_H */

@@ -1,0 +1,1228 @@
+// Host side of the C-ABI (include/countmc_b200.h): the B200 replacement of
+// countmc::GibbsEngine (P:include/countmc/engine.hpp:110-159,
+// P:src/engine.cpp:25-483).  Validation, setup (A = yX, column groups,
+// saved genes, initial states) and output assembly run here in C++; every
+// sweep runs on the device (sweep_kernels.cu), replayed from CUDA graphs,
+// with no per-iteration host round trip.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/countmc_b200.h"
+#include "rng.cuh"
+#include "sweep.h"
+
+using namespace cmc;
+
+namespace {
+
+// ------------------------------------------------------------ NCCL (dlopen)
+typedef struct {
+  char internal[128];
+} nccl_uid;
+typedef void* nccl_comm;
+typedef int (*fn_get_uid)(nccl_uid*);
+typedef int (*fn_init_rank)(nccl_comm*, int, nccl_uid, int);
+typedef int (*fn_all_gather)(const void*, void*, size_t, int, nccl_comm,
+                             cudaStream_t);
+typedef int (*fn_destroy)(nccl_comm);
+typedef const char* (*fn_errstr)(int);
+
+struct NcclApi {
+  void* lib = nullptr;
+  fn_get_uid get_uid = nullptr;
+  fn_init_rank init_rank = nullptr;
+  fn_all_gather all_gather = nullptr;
+  fn_destroy destroy = nullptr;
+  fn_errstr errstr = nullptr;
+  bool load(std::string& why) {
+    if (lib) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) {
+      why = "cannot dlopen libnccl.so.2";
+      return false;
+    }
+    get_uid = (fn_get_uid)dlsym(lib, "ncclGetUniqueId");
+    init_rank = (fn_init_rank)dlsym(lib, "ncclCommInitRank");
+    all_gather = (fn_all_gather)dlsym(lib, "ncclAllGather");
+    destroy = (fn_destroy)dlsym(lib, "ncclCommDestroy");
+    errstr = (fn_errstr)dlsym(lib, "ncclGetErrorString");
+    if (!get_uid || !init_rank || !all_gather || !destroy) {
+      why = "libnccl is missing symbols";
+      return false;
+    }
+    return true;
+  }
+};
+NcclApi g_nccl;
+constexpr int kNcclFloat64 = 8;  // ncclDouble
+
+// ---------------------------------------------------------------- errors
+void set_err(cmc_error* err, int code, const std::string& msg) {
+  if (!err) return;
+  std::memset(err, 0, sizeof(*err));
+  err->code = code;
+  err->index1 = err->index2 = -1;
+  std::snprintf(err->msg, sizeof(err->msg), "%s", msg.c_str());
+}
+
+// SamplerStallError message, P:src/errors.cpp:8-16.
+void set_stall(cmc_error* err, const char* step, long i1, long i2, double x0,
+               double w, long m) {
+  if (!err) return;
+  std::memset(err, 0, sizeof(*err));
+  err->code = CMC_ERR_STALL;
+  std::snprintf(err->step, sizeof(err->step), "%s", step);
+  err->index1 = i1;
+  err->index2 = i2;
+  err->x0 = x0;
+  err->width = w;
+  err->iteration = m;
+  std::snprintf(err->msg, sizeof(err->msg),
+                "slice sampler stalled: step=%s index=(%ld,%ld) x0=%.17g "
+                "width=%.17g iteration=%ld",
+                step[0] ? step : "?", i1, i2, x0, w, m);
+}
+
+#define CUDA_TRY(expr)                                                      \
+  do {                                                                      \
+    cudaError_t e_ = (expr);                                                \
+    if (e_ != cudaSuccess) {                                                \
+      set_err(err, CMC_ERR_CUDA,                                            \
+              std::string(#expr) + ": " + cudaGetErrorString(e_));          \
+      return CMC_ERR_CUDA;                                                  \
+    }                                                                       \
+  } while (0)
+
+long matrix_rank(std::vector<double> A, long n, long m, double tol) {
+  double maxabs = 0.0;
+  for (double v : A) maxabs = std::max(maxabs, std::fabs(v));
+  if (maxabs == 0.0) return 0;
+  const double thresh = tol * maxabs;
+  long rank = 0;
+  for (long col = 0; col < m && rank < n; ++col) {
+    long pivot = rank;
+    for (long r = rank + 1; r < n; ++r)
+      if (std::fabs(A[r * m + col]) > std::fabs(A[pivot * m + col])) pivot = r;
+    if (std::fabs(A[pivot * m + col]) <= thresh) continue;
+    if (pivot != rank)
+      for (long c = 0; c < m; ++c) std::swap(A[pivot * m + c], A[rank * m + c]);
+    for (long r = rank + 1; r < n; ++r) {
+      const double f = A[r * m + col] / A[rank * m + col];
+      for (long c = col; c < m; ++c) A[r * m + c] -= f * A[rank * m + c];
+    }
+    ++rank;
+  }
+  return rank;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t alloc(size_t count) {
+    n = count;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc(&p, sizeof(T) * count);
+  }
+  void free_() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct cmc_engine {
+  // problem (host copy of the full problem)
+  long G_total = 0, N = 0, L = 0;
+  std::vector<long long> counts;  // G x N
+  std::vector<double> X, h, c, s;
+  double a = 1, b = 1, d = 1000;
+  cmc_run_config cfg{};
+  // column groups, P:src/engine.cpp:62-75
+  std::vector<int> grp_off, grp_moff, grp_mem;
+  std::vector<double> grp_val;
+  int Jmax = 1;
+  std::vector<long> saved;  // global, ascending
+  // contrasts
+  ContrastTable ctab{};
+  bool has_ctab = false;
+  // sharding
+  int rank = 0, world = 1;
+  long g0 = 0, G = 0;  // local range
+  nccl_comm comm = nullptr;
+  // device
+  int device = 0;
+  bool dev_ready = false;
+  cudaStream_t stream = nullptr;
+  int C = 1;
+  DevBuf<double> y, A, Xd, hd, gval;
+  DevBuf<int> goff, gmoff, gmem, saved_slot;
+  DevBuf<double> eps, eps_w, eps_wa, gam, gam_w, gam_wa, beta, beta_w, beta_wa;
+  DevBuf<double> log_gam, inv_gam, acc_eps, acc_gam, acc_beta, cprob, samples;
+  DevBuf<double> partA, partB, stall_x0, stall_w;
+  DevBuf<Hyper> hyper;
+  DevBuf<ContrastTable> dctab;
+  DevBuf<long> d_m;
+  long host_m = 1;  // value of *d_m
+  SweepParams base{};
+  // graph cache: chunk length -> exec
+  cudaGraphExec_t graph = nullptr;
+  long graph_len = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timing_pending = false;
+  double sweep_seconds = 0.0;
+  bool begun = false;
+  long n_cols = 0, n_rows = 0;
+};
+
+namespace {
+
+int fail_config(cmc_error* err, const std::string& msg) {
+  set_err(err, CMC_ERR_CONFIG, msg);
+  return CMC_ERR_CONFIG;
+}
+
+long prob_len(const cmc_engine* e) { return e->has_ctab ? e->ctab.n_prob : 0; }
+
+// Allocate and upload this shard's problem and all chain state.
+int ensure_device(cmc_engine* e, cmc_error* err) {
+  if (e->dev_ready) return CMC_OK;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreate(&e->ev0));
+  CUDA_TRY(cudaEventCreate(&e->ev1));
+  const long G = e->G, N = e->N, L = e->L, C = e->C;
+  const int Q = 2 + (int)L;
+  // SoA y[n][g] as double (exact for counts < 2^53)
+  std::vector<double> yh((size_t)N * G);
+  for (long g = 0; g < G; ++g)
+    for (long n = 0; n < N; ++n)
+      yh[(size_t)n * G + g] = (double)e->counts[(size_t)(e->g0 + g) * N + n];
+  CUDA_TRY(e->y.alloc(yh.size()));
+  CUDA_TRY(cudaMemcpy(e->y.p, yh.data(), sizeof(double) * yh.size(),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(e->Xd.alloc(e->X.size()));
+  CUDA_TRY(cudaMemcpy(e->Xd.p, e->X.data(), sizeof(double) * e->X.size(),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(e->hd.alloc(e->h.size()));
+  CUDA_TRY(cudaMemcpy(e->hd.p, e->h.data(), sizeof(double) * e->h.size(),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(e->A.alloc((size_t)L * G));
+  CUDA_TRY(launch_compute_A(e->y.p, e->Xd.p, e->A.p, (int)G, (int)N, (int)L,
+                            e->stream));
+  CUDA_TRY(e->goff.alloc(e->grp_off.size()));
+  CUDA_TRY(cudaMemcpy(e->goff.p, e->grp_off.data(), sizeof(int) * e->grp_off.size(),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(e->gmoff.alloc(e->grp_moff.size()));
+  CUDA_TRY(cudaMemcpy(e->gmoff.p, e->grp_moff.data(),
+                      sizeof(int) * e->grp_moff.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(e->gmem.alloc(std::max<size_t>(1, e->grp_mem.size())));
+  if (!e->grp_mem.empty())
+    CUDA_TRY(cudaMemcpy(e->gmem.p, e->grp_mem.data(),
+                        sizeof(int) * e->grp_mem.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(e->gval.alloc(std::max<size_t>(1, e->grp_val.size())));
+  if (!e->grp_val.empty())
+    CUDA_TRY(cudaMemcpy(e->gval.p, e->grp_val.data(),
+                        sizeof(double) * e->grp_val.size(), cudaMemcpyHostToDevice));
+  std::vector<int> slot((size_t)G, -1);
+  for (size_t k = 0; k < e->saved.size(); ++k) {
+    const long g = e->saved[k] - e->g0;
+    if (g >= 0 && g < G) slot[(size_t)g] = (int)k;
+  }
+  CUDA_TRY(e->saved_slot.alloc(slot.size()));
+  CUDA_TRY(cudaMemcpy(e->saved_slot.p, slot.data(), sizeof(int) * slot.size(),
+                      cudaMemcpyHostToDevice));
+  // chain state
+  const size_t gn = (size_t)G * N * C, gl = (size_t)G * L * C, gc = (size_t)G * C;
+  CUDA_TRY(e->eps.alloc(gn));
+  CUDA_TRY(e->eps_w.alloc(gn));
+  CUDA_TRY(e->eps_wa.alloc(gn));
+  CUDA_TRY(e->gam.alloc(gc));
+  CUDA_TRY(e->gam_w.alloc(gc));
+  CUDA_TRY(e->gam_wa.alloc(gc));
+  CUDA_TRY(e->beta.alloc(gl));
+  CUDA_TRY(e->beta_w.alloc(gl));
+  CUDA_TRY(e->beta_wa.alloc(gl));
+  CUDA_TRY(e->log_gam.alloc(gc));
+  CUDA_TRY(e->inv_gam.alloc(gc));
+  CUDA_TRY(e->acc_eps.alloc(4 * gn));
+  CUDA_TRY(e->acc_gam.alloc(4 * gc));
+  CUDA_TRY(e->acc_beta.alloc(4 * gl));
+  CUDA_TRY(e->cprob.alloc(std::max<long>(1, prob_len(e)) * C));
+  CUDA_TRY(e->samples.alloc(std::max<long>(1, e->n_cols * e->n_rows) * C));
+  CUDA_TRY(e->stall_x0.alloc(gc));
+  CUDA_TRY(e->stall_w.alloc(gc));
+  CUDA_TRY(e->hyper.alloc((size_t)C));
+  CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * C));
+  const long n_leaves_total = (e->G_total + kLeaf - 1) / kLeaf;
+  const long lpr = (n_leaves_total + e->world - 1) / e->world;
+  CUDA_TRY(e->partA.alloc((size_t)e->world * C * Q * lpr));
+  CUDA_TRY(e->partB.alloc((size_t)e->world * C * L * lpr));
+  CUDA_TRY(e->dctab.alloc(1));
+  CUDA_TRY(cudaMemcpy(e->dctab.p, &e->ctab, sizeof(ContrastTable),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(e->d_m.alloc(1));
+  long one = 1;
+  CUDA_TRY(cudaMemcpy(e->d_m.p, &one, sizeof(long), cudaMemcpyHostToDevice));
+  e->host_m = 1;
+
+  SweepParams& p = e->base;
+  std::memset(&p, 0, sizeof(p));
+  p.G = (int)G;
+  p.N = (int)N;
+  p.L = (int)L;
+  p.g0 = e->g0;
+  p.G_total = e->G_total;
+  p.n_leaves_local = (int)((G + kLeaf - 1) / kLeaf);
+  p.n_leaves_total = (int)n_leaves_total;
+  p.leaves_per_rank = (int)lpr;
+  p.world = e->world;
+  p.Jmax = e->Jmax;
+  p.fuse_tail = e->world == 1 ? 1 : 0;
+  p.y = e->y.p;
+  p.A = e->A.p;
+  p.X = e->Xd.p;
+  p.h = e->hd.p;
+  p.grp_off = e->goff.p;
+  p.grp_val = e->gval.p;
+  p.grp_moff = e->gmoff.p;
+  p.grp_mem = e->gmem.p;
+  p.a = e->a;
+  p.b = e->b;
+  p.d = e->d;
+  for (long l = 0; l < L; ++l) {
+    p.c[l] = e->c[l];
+    p.s[l] = e->s[l];
+  }
+  p.exp_clamp = std::exp(700.0);
+  p.seed = e->cfg.seed;
+  p.K = e->cfg.max_step_out;
+  p.max_shrink = e->cfg.max_shrink;
+  p.burnin = e->cfg.burnin;
+  p.tune_cutoff = e->cfg.tune_cutoff;
+  p.thin = e->cfg.thin;
+  p.n_rows = e->n_rows;
+  p.n_cols = e->n_cols;
+  p.n_saved = (long)e->saved.size();
+  p.direct = e->cfg.sampler_mode == CMC_CONJUGATE_DIRECT;
+  p.d_m = e->d_m.p;
+  p.eps = e->eps.p;
+  p.eps_w = e->eps_w.p;
+  p.eps_wa = e->eps_wa.p;
+  p.gam = e->gam.p;
+  p.gam_w = e->gam_w.p;
+  p.gam_wa = e->gam_wa.p;
+  p.beta = e->beta.p;
+  p.beta_w = e->beta_w.p;
+  p.beta_wa = e->beta_wa.p;
+  p.log_gam = e->log_gam.p;
+  p.inv_gam = e->inv_gam.p;
+  p.hyper = e->hyper.p;
+  p.acc_eps = e->acc_eps.p;
+  p.acc_gam = e->acc_gam.p;
+  p.acc_beta = e->acc_beta.p;
+  p.cprob = e->cprob.p;
+  p.ctab = e->dctab.p;
+  p.ctab_n = e->has_ctab ? e->ctab.n : 0;
+  p.ctab_gene_in_sweep = e->has_ctab && !e->ctab.gene_needs_hyper;
+  p.samples = e->samples.p;
+  p.saved_slot = e->saved_slot.p;
+  p.partA = e->partA.p;
+  p.partB = e->partB.p;
+  p.C = (int)C;
+  p.stall_x0 = e->stall_x0.p;
+  p.stall_w = e->stall_w.p;
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->dev_ready = true;
+  return CMC_OK;
+}
+
+// GibbsEngine::initial_state, P:src/engine.cpp:98-142 (host, glibc libm:
+// bit-identical to the reference on the same machine).
+void initial_state_host(const cmc_engine* e, long chain, double* st) {
+  const long G = e->G_total, N = e->N, L = e->L;
+  double* eps = st;
+  double* gam = eps + G * N;
+  double* beta = gam + G;
+  double* theta = beta + G * L;
+  double* sigma = theta + L;
+  std::fill(eps, eps + G * N, 0.0);
+  std::fill(gam, gam + G, 1.0);
+  std::fill(beta, beta + G * L, 0.0);
+  std::fill(theta, theta + L, 0.0);
+  std::fill(sigma, sigma + L, 1.0);
+  double& nu = sigma[L];
+  double& tau = sigma[L + 1];
+  nu = 2.0;
+  tau = 1.0;
+  double hbar = 0.0;
+  for (double v : e->h) hbar += v;
+  hbar /= (double)N;
+  for (long g = 0; g < G; ++g) {
+    double mean = 0.0;
+    for (long n = 0; n < N; ++n) mean += (double)e->counts[(size_t)g * N + n];
+    mean /= (double)N;
+    beta[g * L] = std::log(mean + 1.0) - hbar;
+  }
+  double tbar = 0.0;
+  for (long g = 0; g < G; ++g) tbar += beta[g * L];
+  theta[0] = tbar / (double)G;
+  if (chain > 0) {
+    const uint64_t seed = e->cfg.seed, ch = (uint64_t)chain;
+    auto z = [&](uint64_t fam, uint64_t flat) {
+      Stream s;
+      s.init(seed, ch, 0, site_id(fam, flat));
+      return 0.5 * normal(s);
+    };
+    auto clamp_interior = [](double v, double lo, double hi) {
+      return std::min(std::max(v, lo), hi);
+    };
+    for (long g = 0; g < G; ++g) {
+      for (long n = 0; n < N; ++n) eps[g * N + n] += z(kSiteEps, (uint64_t)(g * N + n));
+      gam[g] = std::max(1e-3, gam[g] + z(kSiteGamma, (uint64_t)g));
+      for (long l = 0; l < L; ++l) beta[g * L + l] += z(kSiteBeta, (uint64_t)(g * L + l));
+    }
+    for (long l = 0; l < L; ++l) {
+      theta[l] += z(kSiteTheta, (uint64_t)l);
+      const double sv = e->s[l];
+      sigma[l] = clamp_interior(sigma[l] + z(kSiteSigma, (uint64_t)l), 1e-6 * sv,
+                                (1.0 - 1e-6) * sv);
+    }
+    nu = clamp_interior(nu + z(kSiteNu, 0), 1e-6 * e->d, (1.0 - 1e-6) * e->d);
+    tau = std::max(1e-3, tau + z(kSiteTau, 0));
+  }
+}
+
+// Upload one chain's packed state (+ optional tuning) into slot `c`.
+int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
+                 const double* ta, cmc_error* err) {
+  const long Gt = e->G_total, G = e->G, N = e->N, L = e->L, g0 = e->g0;
+  const double* eps = st;
+  const double* gam = eps + Gt * N;
+  const double* beta = gam + Gt;
+  const double* theta = beta + Gt * L;
+  const double* sigma = theta + L;
+  std::vector<double> buf((size_t)std::max(N, L) * G);
+  auto put_gn = [&](const double* src, double* dst, long K) -> cudaError_t {
+    for (long k = 0; k < K; ++k)
+      for (long g = 0; g < G; ++g) buf[(size_t)k * G + g] = src[(g0 + g) * K + k];
+    return cudaMemcpy(dst, buf.data(), sizeof(double) * K * G, cudaMemcpyHostToDevice);
+  };
+  const size_t so = (size_t)c;
+  CUDA_TRY(put_gn(eps, e->eps.p + so * N * G, N));
+  CUDA_TRY(cudaMemcpy(e->gam.p + so * G, gam + g0, sizeof(double) * G,
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(put_gn(beta, e->beta.p + so * L * G, L));
+  if (tw && ta) {
+    const double* tws[2] = {tw, ta};
+    double* de[2] = {e->eps_w.p, e->eps_wa.p};
+    double* dg[2] = {e->gam_w.p, e->gam_wa.p};
+    double* db[2] = {e->beta_w.p, e->beta_wa.p};
+    for (int k = 0; k < 2; ++k) {
+      const double* t = tws[k];
+      CUDA_TRY(put_gn(t, de[k] + so * N * G, N));
+      CUDA_TRY(cudaMemcpy(dg[k] + so * G, t + Gt * N + g0, sizeof(double) * G,
+                          cudaMemcpyHostToDevice));
+      CUDA_TRY(put_gn(t + Gt * N + Gt, db[k] + so * L * G, L));
+    }
+  }
+  Hyper hp;
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + c, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  hp.nu = sigma[L];
+  hp.tau = sigma[L + 1];
+  for (long l = 0; l < L; ++l) {
+    hp.theta[l] = theta[l];
+    hp.sigma[l] = sigma[l];
+  }
+  if (tw && ta) {
+    const long off = Gt * N + Gt + Gt * L;
+    for (long l = 0; l < L; ++l) {
+      hp.w_sigma[l] = tw[off + l];
+      hp.wa_sigma[l] = ta[off + l];
+    }
+    hp.w_nu = tw[off + L];
+    hp.wa_nu = ta[off + L];
+    hp.w_tau = tw[off + L + 1];
+    hp.wa_tau = ta[off + L + 1];
+  }
+  hp.err_key = kNoError;
+  hp.doneA = hp.doneB = 0;
+  CUDA_TRY(cudaMemcpy(e->hyper.p + c, &hp, sizeof(Hyper), cudaMemcpyHostToDevice));
+  return CMC_OK;
+}
+
+int download_state(cmc_engine* e, long c, double* st, double* tw, double* ta,
+                   cmc_error* err) {
+  const long Gt = e->G_total, G = e->G, N = e->N, L = e->L, g0 = e->g0;
+  std::vector<double> buf((size_t)std::max(N, L) * G);
+  auto get_gn = [&](const double* src, double* dst, long K) -> cudaError_t {
+    cudaError_t r = cudaMemcpy(buf.data(), src, sizeof(double) * K * G,
+                               cudaMemcpyDeviceToHost);
+    if (r != cudaSuccess) return r;
+    for (long k = 0; k < K; ++k)
+      for (long g = 0; g < G; ++g) dst[(g0 + g) * K + k] = buf[(size_t)k * G + g];
+    return cudaSuccess;
+  };
+  const size_t so = (size_t)c;
+  Hyper hp;
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + c, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  if (st) {
+    double* eps = st;
+    double* gam = eps + Gt * N;
+    double* beta = gam + Gt;
+    double* theta = beta + Gt * L;
+    double* sigma = theta + L;
+    CUDA_TRY(get_gn(e->eps.p + so * N * G, eps, N));
+    CUDA_TRY(cudaMemcpy(gam + g0, e->gam.p + so * G, sizeof(double) * G,
+                        cudaMemcpyDeviceToHost));
+    CUDA_TRY(get_gn(e->beta.p + so * L * G, beta, L));
+    for (long l = 0; l < L; ++l) {
+      theta[l] = hp.theta[l];
+      sigma[l] = hp.sigma[l];
+    }
+    sigma[L] = hp.nu;
+    sigma[L + 1] = hp.tau;
+  }
+  double* tws[2] = {tw, ta};
+  double* de[2] = {e->eps_w.p, e->eps_wa.p};
+  double* dg[2] = {e->gam_w.p, e->gam_wa.p};
+  double* db[2] = {e->beta_w.p, e->beta_wa.p};
+  for (int k = 0; k < 2; ++k) {
+    double* t = tws[k];
+    if (!t) continue;
+    CUDA_TRY(get_gn(de[k] + so * N * G, t, N));
+    CUDA_TRY(cudaMemcpy(t + Gt * N + g0, dg[k] + so * G, sizeof(double) * G,
+                        cudaMemcpyDeviceToHost));
+    CUDA_TRY(get_gn(db[k] + so * L * G, t + Gt * N + Gt, L));
+    const long off = Gt * N + Gt + Gt * L;
+    for (long l = 0; l < L; ++l) t[off + l] = k == 0 ? hp.w_sigma[l] : hp.wa_sigma[l];
+    t[off + L] = k == 0 ? hp.w_nu : hp.wa_nu;
+    t[off + L + 1] = k == 0 ? hp.w_tau : hp.wa_tau;
+  }
+  return CMC_OK;
+}
+
+// Decode the device stall record of the lowest stalled chain slot.
+int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
+  for (long c = slot_lo; c < slot_hi; ++c) {
+    Hyper hp;
+    CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + c, sizeof(Hyper), cudaMemcpyDeviceToHost));
+    if (hp.err_key == kNoError) continue;
+    const unsigned step = (unsigned)(hp.err_key >> 60);
+    const long col = (long)((hp.err_key >> 52) & 0xff);
+    const long g = (long)((hp.err_key >> 20) & 0xffffffffull);
+    const long n = (long)(hp.err_key & 0xfffff);
+    double x0 = 0, w = 0;
+    if (step == 1 || step == 2 || step == 5) {
+      const long gl = g - e->g0;
+      CUDA_TRY(cudaMemcpy(&x0, e->stall_x0.p + c * e->G + gl, sizeof(double),
+                          cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(&w, e->stall_w.p + c * e->G + gl, sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    } else {
+      const int k = step == 3 ? 0 : step == 4 ? 1 : 2 + (int)col;
+      x0 = hp.err_x0[k];
+      w = hp.err_w[k];
+    }
+    const long it = (long)hp.err_m;
+    switch (step) {
+      case 1: set_stall(err, "epsilon", g + 1, n + 1, x0, w, it); break;
+      case 2: set_stall(err, "gamma", g + 1, -1, x0, w, it); break;
+      case 3: set_stall(err, "nu", -1, -1, x0, w, it); break;
+      case 4: set_stall(err, "tau", -1, -1, x0, w, it); break;
+      case 5: set_stall(err, "beta", g + 1, col + 1, x0, w, it); break;
+      default: set_stall(err, "sigma", col + 1, -1, x0, w, it); break;
+    }
+    return CMC_ERR_STALL;
+  }
+  return CMC_OK;
+}
+
+// Enqueue one sweep (iteration *d_m + off) for grid.y chains at slot_base.
+cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
+                          long off) {
+  cudaError_t r = launch_gene_sweep(p, chains, off, e->stream);
+  if (r != cudaSuccess) return r;
+  if (e->world == 1) {
+    if ((r = launch_leaf_a(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if ((r = launch_leaf_b(p, chains, off, e->stream)) != cudaSuccess) return r;
+  } else {
+    const int Q = 2 + (int)e->L;
+    const size_t cA = (size_t)e->C * Q * p.leaves_per_rank;
+    const size_t cB = (size_t)e->C * e->L * p.leaves_per_rank;
+    if ((r = launch_leaf_a(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if (g_nccl.all_gather(e->partA.p + (size_t)e->rank * cA, e->partA.p, cA,
+                          kNcclFloat64, e->comm, e->stream) != 0)
+      return cudaErrorUnknown;
+    if ((r = launch_hyper_a(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if ((r = launch_leaf_b(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if (g_nccl.all_gather(e->partB.p + (size_t)e->rank * cB, e->partB.p, cB,
+                          kNcclFloat64, e->comm, e->stream) != 0)
+      return cudaErrorUnknown;
+    if ((r = launch_hyper_b(p, chains, off, e->stream)) != cudaSuccess) return r;
+  }
+  if (p.monitor_enabled && e->has_ctab && e->ctab.gene_needs_hyper)
+    if ((r = launch_gene_contrast(p, chains, off, e->stream)) != cudaSuccess) return r;
+  return cudaSuccess;
+}
+
+int set_device_m(cmc_engine* e, long m, cmc_error* err) {
+  if (e->host_m == m) return CMC_OK;
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  CUDA_TRY(cudaMemcpy(e->d_m.p, &m, sizeof(long), cudaMemcpyHostToDevice));
+  e->host_m = m;
+  return CMC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cmc_version(void) {
+  return "countmc_b200 0.1 (sm_100a, fp64, -fmad=false parity build)";
+}
+
+int cmc_shard_bounds(long G, int rank, int world, long* g_begin, long* g_end) {
+  if (world < 1 || rank < 0 || rank >= world || G < 1) return CMC_ERR_ARG;
+  const long leaves = (G + kLeaf - 1) / kLeaf;
+  const long lpr = (leaves + world - 1) / world;
+  const long b = std::min(G, (long)rank * lpr * kLeaf);
+  const long en = std::min(G, (long)(rank + 1) * lpr * kLeaf);
+  *g_begin = b;
+  *g_end = en;
+  return CMC_OK;
+}
+
+int cmc_engine_create(const cmc_problem* p, const cmc_run_config* config,
+                      const cmc_contrast_set* cs, int device, cmc_engine** out,
+                      cmc_error* err) {
+  if (!p || !config || !out) {
+    set_err(err, CMC_ERR_ARG, "null argument");
+    return CMC_ERR_ARG;
+  }
+  *out = nullptr;
+  // CountMatrix::validate / ModelSpec::validate / PriorConfig::validate,
+  // P:src/types.cpp:18-69
+  if (p->G < 1 || p->N < 1)
+    return fail_config(err, "count matrix must have at least one gene and one sample");
+  if (p->L < 1)
+    return fail_config(err, "model matrix must have at least one row and one column");
+  if (!p->counts || !p->X || !p->h || !p->c || !p->s) {
+    set_err(err, CMC_ERR_ARG, "null problem array");
+    return CMC_ERR_ARG;
+  }
+  for (long i = 0; i < p->G * p->N; ++i)
+    if (p->counts[i] < 0) {
+      char buf[128];
+      std::snprintf(buf, sizeof(buf), "negative count at gene %ld, sample %ld",
+                    i / p->N + 1, i % p->N + 1);
+      return fail_config(err, buf);
+    }
+  for (long i = 0; i < p->N; ++i)
+    if (!std::isfinite(p->h[i])) return fail_config(err, "offsets must be finite");
+  for (long i = 0; i < p->N * p->L; ++i)
+    if (!std::isfinite(p->X[i]))
+      return fail_config(err, "model matrix entries must be finite");
+  if (matrix_rank(std::vector<double>(p->X, p->X + p->N * p->L), p->N, p->L, 1e-10) < p->L)
+    return fail_config(err, "model matrix does not have full column rank");
+  if (!(p->a > 0.0) || !(p->b > 0.0) || !(p->d > 0.0))
+    return fail_config(err, "prior constants a, b, d must be strictly positive");
+  for (long l = 0; l < p->L; ++l)
+    if (!(p->c[l] > 0.0) || !(p->s[l] > 0.0))
+      return fail_config(err, "prior entries c, s must be strictly positive");
+  // device limits of this build
+  if (p->L > kLMax) return fail_config(err, "L exceeds the 16 columns this build supports");
+  if (p->N >= (1 << 20)) return fail_config(err, "N too large for this build");
+  if (p->G >= (1L << 32)) return fail_config(err, "G too large for this build");
+  // RunConfig::resolve, P:src/engine.cpp:25-40
+  cmc_run_config cfg = *config;
+  if (cfg.chains < 1) return fail_config(err, "chains must be >= 1");
+  if (cfg.iterations < 1) return fail_config(err, "iterations must be >= 1");
+  if (cfg.burnin < 1) return fail_config(err, "burnin must be >= 1");
+  if (cfg.thin < 1) return fail_config(err, "thin must be >= 1");
+  if (cfg.workers < 1) return fail_config(err, "workers must be >= 1");
+  if (cfg.save_genes < 0) return fail_config(err, "save_genes must be >= 0");
+  if (cfg.max_step_out < 1) return fail_config(err, "max_step_out must be >= 1");
+  if (cfg.tune_cutoff < 0) cfg.tune_cutoff = std::min<long>(500, cfg.burnin / 10);
+  if (cfg.tune_cutoff >= cfg.burnin)
+    return fail_config(err, "tune_cutoff must be less than burnin (M_C < M_B)");
+  if (!(cfg.w_init > 0.0)) return fail_config(err, "w_init must be positive");
+  if (cfg.max_shrink < 1) return fail_config(err, "max_shrink must be >= 1");
+
+  auto* e = new cmc_engine();
+  e->G_total = p->G;
+  e->N = p->N;
+  e->L = p->L;
+  e->counts.assign(p->counts, p->counts + p->G * p->N);
+  e->X.assign(p->X, p->X + p->N * p->L);
+  e->h.assign(p->h, p->h + p->N);
+  e->c.assign(p->c, p->c + p->L);
+  e->s.assign(p->s, p->s + p->L);
+  e->a = p->a;
+  e->b = p->b;
+  e->d = p->d;
+  e->cfg = cfg;
+  e->device = device;
+  e->C = (int)cfg.chains;
+  e->G = p->G;
+  e->g0 = 0;
+
+  // column groups in first-appearance order, P:src/engine.cpp:62-75
+  const long N = p->N, L = p->L;
+  e->grp_off.push_back(0);
+  e->grp_moff.push_back(0);
+  int jmax = 1;
+  for (long l = 0; l < L; ++l) {
+    std::vector<double> vals;
+    std::vector<std::vector<int>> mem;
+    for (long n = 0; n < N; ++n) {
+      const double v = p->X[n * L + l];
+      if (v == 0.0) continue;
+      size_t j = 0;
+      for (; j < vals.size(); ++j)
+        if (vals[j] == v) break;
+      if (j == vals.size()) {
+        vals.push_back(v);
+        mem.emplace_back();
+      }
+      mem[j].push_back((int)n);
+    }
+    for (size_t j = 0; j < vals.size(); ++j) {
+      e->grp_val.push_back(vals[j]);
+      e->grp_mem.insert(e->grp_mem.end(), mem[j].begin(), mem[j].end());
+      e->grp_moff.push_back((int)e->grp_mem.size());
+    }
+    e->grp_off.push_back((int)e->grp_val.size());
+    jmax = std::max<int>(jmax, (int)vals.size());
+  }
+  e->Jmax = jmax;
+
+  // saved genes: partial Fisher-Yates on (seed, 0, 0, kSaveSel), sorted,
+  // P:src/engine.cpp:77-90
+  const long k = std::min<long>(cfg.save_genes, p->G);
+  if (k > 0) {
+    std::vector<long> idx((size_t)p->G);
+    std::iota(idx.begin(), idx.end(), 0L);
+    Stream sel;
+    sel.init(cfg.seed, 0, 0, site_id(kSiteSaveSel, 0));
+    for (long i = 0; i < k; ++i) {
+      const long j = i + (long)sel.uniform_int((uint64_t)(p->G - i));
+      std::swap(idx[(size_t)i], idx[(size_t)j]);
+    }
+    e->saved.assign(idx.begin(), idx.begin() + k);
+    std::sort(e->saved.begin(), e->saved.end());
+  }
+  e->n_cols = 2 + 2 * L + (long)e->saved.size() * (L + 1);
+  e->n_rows = cfg.iterations / cfg.thin;
+
+  // contrasts: ContrastSpec::finalize (P:src/streaming.cpp:76-88) and
+  // parse_param_ref's range check (P:src/streaming.cpp:65-72)
+  if (cs && cs->n_contrasts > 0) {
+    ContrastTable& t = e->ctab;
+    std::memset(&t, 0, sizeof(t));
+    if (cs->n_contrasts > kMaxContrasts) {
+      delete e;
+      return fail_config(err, "too many contrasts for this build (max 8)");
+    }
+    t.n = cs->n_contrasts;
+    int term = 0, q = 0;
+    long off = 0;
+    for (int ci = 0; ci < cs->n_contrasts; ++ci) {
+      t.term_begin[ci] = term;
+      if (cs->n_terms[ci] < 1) {
+        delete e;
+        return fail_config(err, "contrast has no terms");
+      }
+      bool per_gene = false, needs_hyper = false;
+      for (int ti = 0; ti < cs->n_terms[ci]; ++ti, ++term) {
+        if (term >= kMaxTerms) {
+          delete e;
+          return fail_config(err, "too many contrast terms for this build");
+        }
+        t.coef_begin[term] = q;
+        t.threshold[term] = cs->threshold[term];
+        if (cs->n_coefs[term] < 1) {
+          delete e;
+          return fail_config(err, "contrast has a term with no coefficients");
+        }
+        for (int kk = 0; kk < cs->n_coefs[term]; ++kk, ++q) {
+          if (q >= kMaxCoefs) {
+            delete e;
+            return fail_config(err, "too many contrast coefficients for this build");
+          }
+          const int fam = cs->family[q], ix = cs->index[q];
+          if (fam < 0 || fam > 5) {
+            delete e;
+            return fail_config(err, "unknown parameter name in contrast");
+          }
+          if ((fam == CMC_FAM_BETA_COL || fam == CMC_FAM_THETA || fam == CMC_FAM_SIGMA) &&
+              (ix < 0 || ix >= L)) {
+            delete e;
+            return fail_config(err, "contrast index out of range");
+          }
+          t.fam[q] = fam;
+          t.idx[q] = ix;
+          t.coef[q] = cs->coef[q];
+          if (fam == CMC_FAM_BETA_COL || fam == CMC_FAM_GAMMA) per_gene = true;
+          else needs_hyper = true;
+        }
+      }
+      t.per_gene[ci] = per_gene ? 1 : 0;
+      if (per_gene && needs_hyper) t.gene_needs_hyper = 1;
+      t.prob_off[ci] = off;
+      off += per_gene ? p->G : 1;
+    }
+    t.term_begin[cs->n_contrasts] = term;
+    t.coef_begin[term] = q;
+    t.n_prob = off;
+    e->has_ctab = true;
+  }
+  *out = e;
+  return CMC_OK;
+}
+
+int cmc_engine_destroy(cmc_engine* e) {
+  if (!e) return CMC_OK;
+  if (e->dev_ready) {
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->stream);
+    if (e->graph) cudaGraphExecDestroy(e->graph);
+    DevBuf<double>* ds[] = {&e->y, &e->A, &e->Xd, &e->hd, &e->gval, &e->eps,
+                            &e->eps_w, &e->eps_wa, &e->gam, &e->gam_w,
+                            &e->gam_wa, &e->beta, &e->beta_w, &e->beta_wa,
+                            &e->log_gam, &e->inv_gam, &e->acc_eps, &e->acc_gam,
+                            &e->acc_beta, &e->cprob, &e->samples, &e->partA,
+                            &e->partB, &e->stall_x0, &e->stall_w};
+    for (auto* b : ds) b->free_();
+    e->goff.free_();
+    e->gmoff.free_();
+    e->gmem.free_();
+    e->saved_slot.free_();
+    e->hyper.free_();
+    e->dctab.free_();
+    e->d_m.free_();
+    if (e->ev0) cudaEventDestroy(e->ev0);
+    if (e->ev1) cudaEventDestroy(e->ev1);
+    cudaStreamDestroy(e->stream);
+  }
+  if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
+  delete e;
+  return CMC_OK;
+}
+
+int cmc_engine_dims(const cmc_engine* e, long* G, long* N, long* L,
+                    long* chains, long* n_saved, long* n_cols, long* n_rows) {
+  if (!e) return CMC_ERR_ARG;
+  if (G) *G = e->G_total;
+  if (N) *N = e->N;
+  if (L) *L = e->L;
+  if (chains) *chains = e->C;
+  if (n_saved) *n_saved = (long)e->saved.size();
+  if (n_cols) *n_cols = e->n_cols;
+  if (n_rows) *n_rows = e->n_rows;
+  return CMC_OK;
+}
+
+int cmc_engine_saved_genes(const cmc_engine* e, long* out) {
+  if (!e || !out) return CMC_ERR_ARG;
+  std::copy(e->saved.begin(), e->saved.end(), out);
+  return CMC_OK;
+}
+
+int cmc_engine_config(const cmc_engine* e, cmc_run_config* out) {
+  if (!e || !out) return CMC_ERR_ARG;
+  *out = e->cfg;
+  return CMC_OK;
+}
+
+int cmc_engine_initial_state(const cmc_engine* e, long chain, double* state,
+                             cmc_error* err) {
+  if (!e || !state || chain < 0) {
+    set_err(err, CMC_ERR_ARG, "bad argument");
+    return CMC_ERR_ARG;
+  }
+  initial_state_host(e, chain, state);
+  return CMC_OK;
+}
+
+int cmc_engine_set_state(cmc_engine* e, long chain, const double* state,
+                         const double* tw, const double* ta, cmc_error* err) {
+  if (!e || !state || chain < 0 || chain >= e->C) {
+    set_err(err, CMC_ERR_ARG, "bad chain or state");
+    return CMC_ERR_ARG;
+  }
+  int rc = ensure_device(e, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return upload_state(e, chain, state, tw, ta, err);
+}
+
+int cmc_engine_get_state(cmc_engine* e, long chain, double* state, double* tw,
+                         double* ta, cmc_error* err) {
+  if (!e || chain < 0 || chain >= e->C) {
+    set_err(err, CMC_ERR_ARG, "bad chain");
+    return CMC_ERR_ARG;
+  }
+  int rc = ensure_device(e, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  return download_state(e, chain, state, tw, ta, err);
+}
+
+int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
+                       cmc_error* err) {
+  if (!e || chain < 0 || chain >= e->C || m < 1) {
+    set_err(err, CMC_ERR_ARG, "bad chain or iteration");
+    return CMC_ERR_ARG;
+  }
+  int rc = ensure_device(e, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(e->device));
+  if ((rc = set_device_m(e, m, err))) return rc;
+  Hyper hp;
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + chain, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  const unsigned long long before = hp.clamps;
+  hp.err_key = kNoError;
+  CUDA_TRY(cudaMemcpy(&e->hyper.p[chain].err_key, &hp.err_key,
+                      sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  SweepParams p = e->base;
+  p.slot_base = (int)chain;
+  p.chain_base = (int)chain;
+  p.monitor_enabled = 0;
+  CUDA_TRY(enqueue_sweep(e, p, 1, 0));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + chain, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  if (clamps) *clamps += hp.clamps - before;
+  if (hp.err_key != kNoError) return check_stall(e, chain, chain + 1, err);
+  return CMC_OK;
+}
+
+int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
+  if (!e) return CMC_ERR_ARG;
+  int rc = ensure_device(e, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  const long S = e->G_total * e->N + e->G_total + e->G_total * e->L + 2 * e->L + 2;
+  const long T = e->G_total * e->N + e->G_total + e->G_total * e->L + e->L + 2;
+  std::vector<double> st((size_t)S), tw((size_t)T, e->cfg.w_init), ta((size_t)T, 0.0);
+  CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * e->C));
+  for (long c = 0; c < e->C; ++c) {
+    initial_state_host(e, c, st.data());
+    if ((rc = upload_state(e, c, st.data(), tw.data(), ta.data(), err))) return rc;
+  }
+  CUDA_TRY(cudaMemset(e->acc_eps.p, 0, sizeof(double) * e->acc_eps.n));
+  CUDA_TRY(cudaMemset(e->acc_gam.p, 0, sizeof(double) * e->acc_gam.n));
+  CUDA_TRY(cudaMemset(e->acc_beta.p, 0, sizeof(double) * e->acc_beta.n));
+  CUDA_TRY(cudaMemset(e->cprob.p, 0, sizeof(double) * e->cprob.n));
+  CUDA_TRY(cudaMemset(e->samples.p, 0, sizeof(double) * e->samples.n));
+  long one = 1;
+  CUDA_TRY(cudaMemcpy(e->d_m.p, &one, sizeof(long), cudaMemcpyHostToDevice));
+  e->host_m = 1;
+  e->sweep_seconds = 0.0;
+  e->begun = true;
+  return CMC_OK;
+}
+
+int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
+  if (!e || m_begin < 1 || m_end < m_begin) {
+    set_err(err, CMC_ERR_ARG, "bad iteration range");
+    return CMC_ERR_ARG;
+  }
+  if (!e->begun) {
+    set_err(err, CMC_ERR_ARG, "cmc_engine_begin must be called first");
+    return CMC_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(e->device));
+  int rc = set_device_m(e, m_begin, err);
+  if (rc) return rc;
+  SweepParams p = e->base;
+  p.slot_base = 0;
+  p.chain_base = 0;
+  p.monitor_enabled = 1;
+  const long total = m_end - m_begin;
+  const long chunk = 25;
+  CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
+  long done = 0;
+  if (total >= chunk) {
+    if (!e->graph || e->graph_len != chunk) {
+      if (e->graph) cudaGraphExecDestroy(e->graph);
+      e->graph = nullptr;
+      cudaGraph_t g;
+      CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+      for (long off = 0; off < chunk; ++off) {
+        cudaError_t r = enqueue_sweep(e, p, e->C, off);
+        if (r != cudaSuccess) {
+          cudaStreamEndCapture(e->stream, &g);
+          CUDA_TRY(r);
+        }
+      }
+      CUDA_TRY(launch_advance(e->d_m.p, chunk, e->stream));
+      CUDA_TRY(cudaStreamEndCapture(e->stream, &g));
+      CUDA_TRY(cudaGraphInstantiate(&e->graph, g, 0));
+      cudaGraphDestroy(g);
+      e->graph_len = chunk;
+    }
+    for (; done + chunk <= total; done += chunk)
+      CUDA_TRY(cudaGraphLaunch(e->graph, e->stream));
+  }
+  const long rest = total - done;
+  for (long off = 0; off < rest; ++off) CUDA_TRY(enqueue_sweep(e, p, e->C, off));
+  if (rest) CUDA_TRY(launch_advance(e->d_m.p, rest, e->stream));
+  CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+  e->timing_pending = true;
+  e->host_m = m_end;
+  return CMC_OK;
+}
+
+int cmc_engine_sync(cmc_engine* e, cmc_error* err) {
+  if (!e) return CMC_ERR_ARG;
+  if (!e->dev_ready) return CMC_OK;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  if (e->timing_pending) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    e->sweep_seconds += ms * 1e-3;
+    e->timing_pending = false;
+  }
+  return check_stall(e, 0, e->C, err);
+}
+
+int cmc_engine_run(cmc_engine* e, cmc_error* err) {
+  int rc = cmc_engine_begin(e, err);
+  if (rc) return rc;
+  const long total = e->cfg.burnin + e->cfg.iterations;
+  if ((rc = cmc_engine_sweeps(e, 1, total + 1, err))) return rc;
+  return cmc_engine_sync(e, err);
+}
+
+void* cmc_engine_stream(cmc_engine* e) {
+  if (!e) return nullptr;
+  cmc_error err;
+  if (ensure_device(e, &err)) return nullptr;
+  return (void*)e->stream;
+}
+
+int cmc_engine_launches_per_sweep(const cmc_engine* e) {
+  if (!e) return 0;
+  int n = e->world == 1 ? 3 : 5;
+  if (e->has_ctab && e->ctab.gene_needs_hyper) ++n;
+  return n;
+}
+
+int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,
+                          cmc_error* err) {
+  if (!e || !o || chain < 0 || chain >= e->C) {
+    set_err(err, CMC_ERR_ARG, "bad chain");
+    return CMC_ERR_ARG;
+  }
+  int rc = ensure_device(e, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  const long Gt = e->G_total, G = e->G, N = e->N, L = e->L, g0 = e->g0;
+  const size_t so = (size_t)chain;
+  Hyper hp;
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + chain, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  const long count = std::max<long>(0, std::min(e->host_m - 1, e->cfg.burnin + e->cfg.iterations) - e->cfg.burnin);
+  if (o->acc_count) *o->acc_count = count;
+  double* outs[4] = {o->acc_mean, o->acc_meansq, o->acc_mean_c, o->acc_meansq_c};
+  std::vector<double> buf;
+  for (int k = 0; k < 4; ++k) {
+    double* dst = outs[k];
+    if (!dst) continue;
+    long i = 0;
+    dst[i++] = hp.acc[k][0];
+    dst[i++] = hp.acc[k][1];
+    for (long l = 0; l < L; ++l) dst[i++] = hp.acc[k][2 + l];
+    for (long l = 0; l < L; ++l) dst[i++] = hp.acc[k][2 + L + l];
+    // beta G x L
+    buf.resize((size_t)L * G);
+    CUDA_TRY(cudaMemcpy(buf.data(), e->acc_beta.p + so * 4 * L * G + (size_t)k * L * G,
+                        sizeof(double) * L * G, cudaMemcpyDeviceToHost));
+    for (long g = 0; g < G; ++g)
+      for (long l = 0; l < L; ++l) dst[i + (g0 + g) * L + l] = buf[(size_t)l * G + g];
+    i += Gt * L;
+    buf.resize((size_t)G);
+    CUDA_TRY(cudaMemcpy(buf.data(), e->acc_gam.p + so * 4 * G + (size_t)k * G,
+                        sizeof(double) * G, cudaMemcpyDeviceToHost));
+    for (long g = 0; g < G; ++g) dst[i + g0 + g] = buf[(size_t)g];
+    i += Gt;
+    buf.resize((size_t)N * G);
+    CUDA_TRY(cudaMemcpy(buf.data(), e->acc_eps.p + so * 4 * N * G + (size_t)k * N * G,
+                        sizeof(double) * N * G, cudaMemcpyDeviceToHost));
+    for (long g = 0; g < G; ++g)
+      for (long n = 0; n < N; ++n) dst[i + (g0 + g) * N + n] = buf[(size_t)n * G + g];
+  }
+  if (e->has_ctab) {
+    if (o->contrast_prob)
+      CUDA_TRY(cudaMemcpy(o->contrast_prob, e->cprob.p + so * e->ctab.n_prob,
+                          sizeof(double) * e->ctab.n_prob, cudaMemcpyDeviceToHost));
+    if (o->contrast_count)
+      for (int ci = 0; ci < e->ctab.n; ++ci) o->contrast_count[ci] = count;
+  }
+  const long rows = std::min<long>(e->n_rows, count / e->cfg.thin);
+  if (o->samples && e->n_cols * e->n_rows > 0) {
+    buf.resize((size_t)e->n_cols * e->n_rows);
+    CUDA_TRY(cudaMemcpy(buf.data(), e->samples.p + so * e->n_cols * e->n_rows,
+                        sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+    // the reference keeps only completed rows: samples[col].size() == rows
+    for (long c = 0; c < e->n_cols; ++c)
+      for (long r = 0; r < rows; ++r) o->samples[c * rows + r] = buf[(size_t)c * e->n_rows + r];
+  }
+  if (o->sample_iters)
+    for (long r = 0; r < rows; ++r) o->sample_iters[r] = e->cfg.burnin + (r + 1) * e->cfg.thin;
+  if (o->clamp_events) *o->clamp_events = hp.clamps;
+  if (o->final_state) {
+    if ((rc = download_state(e, chain, o->final_state, nullptr, nullptr, err))) return rc;
+  }
+  if (o->step_seconds) {
+    for (int k = 0; k < 7; ++k) o->step_seconds[k] = 0.0;
+    o->step_seconds[0] = e->sweep_seconds;
+  }
+  return CMC_OK;
+}
+
+int cmc_nccl_unique_id(void* out128, cmc_error* err) {
+  std::string why;
+  if (!g_nccl.load(why)) {
+    set_err(err, CMC_ERR_NCCL, why);
+    return CMC_ERR_NCCL;
+  }
+  nccl_uid id;
+  if (g_nccl.get_uid(&id) != 0) {
+    set_err(err, CMC_ERR_NCCL, "ncclGetUniqueId failed");
+    return CMC_ERR_NCCL;
+  }
+  std::memcpy(out128, &id, sizeof(id));
+  return CMC_OK;
+}
+
+int cmc_engine_shard(cmc_engine* e, int rank, int world, const void* uid,
+                     cmc_error* err) {
+  if (!e || world < 1 || rank < 0 || rank >= world) {
+    set_err(err, CMC_ERR_ARG, "bad rank/world");
+    return CMC_ERR_ARG;
+  }
+  if (e->dev_ready) {
+    set_err(err, CMC_ERR_ARG, "cmc_engine_shard must precede device use");
+    return CMC_ERR_ARG;
+  }
+  long b = 0, en = 0;
+  cmc_shard_bounds(e->G_total, rank, world, &b, &en);
+  if (en <= b) {
+    set_err(err, CMC_ERR_CONFIG, "shard has no genes: use fewer ranks for this G");
+    return CMC_ERR_CONFIG;
+  }
+  e->rank = rank;
+  e->world = world;
+  e->g0 = b;
+  e->G = en - b;
+  if (world > 1) {
+    std::string why;
+    if (!g_nccl.load(why)) {
+      set_err(err, CMC_ERR_NCCL, why);
+      return CMC_ERR_NCCL;
+    }
+    CUDA_TRY(cudaSetDevice(e->device));
+    nccl_uid id;
+    std::memcpy(&id, uid, sizeof(id));
+    if (g_nccl.init_rank(&e->comm, world, id, rank) != 0) {
+      set_err(err, CMC_ERR_NCCL, "ncclCommInitRank failed");
+      return CMC_ERR_NCCL;
+    }
+  }
+  return CMC_OK;
+}
+
+// ------------------------------------------------------- synthetic inputs
+
+namespace {
+// Poisson(lambda) from the stream: inversion for small means, Hoermann's
+// PTRS transformed rejection for large ones.
+long long poisson_draw(Stream& s, double lam) {
+  if (lam < 10.0) {
+    const double L = std::exp(-lam);
+    long long k = 0;
+    double p = s.u01();
+    while (p > L) {
+      ++k;
+      p *= s.u01();
+    }
+    return k;
+  }
+  const double slam = std::sqrt(lam), loglam = std::log(lam);
+  const double b = 0.931 + 2.53 * slam;
+  const double a = -0.059 + 0.02483 * b;
+  const double inv_alpha = 1.1239 + 1.1328 / (b - 3.4);
+  const double vr = 0.9277 - 3.6224 / (b - 2.0);
+  for (;;) {
+    const double U = s.u01() - 0.5;
+    const double V = s.u01();
+    const double us = 0.5 - std::fabs(U);
+    const long long k = (long long)std::floor((2.0 * a / us + b) * U + lam + 0.43);
+    if (us >= 0.07 && V <= vr) return k;
+    if (k < 0 || (us < 0.013 && V > us)) continue;
+    if (std::log(V) + std::log(inv_alpha) - std::log(a / (us * us) + b) <=
+        -lam + (double)k * loglam - std::lgamma((double)k + 1.0))
+      return k;
+  }
+}
+}  // namespace
+
+int cmc_simulate(long G, long N, long L, const double* X, const double* h,
+                 double nu, double tau, const double* theta,
+                 const double* sigma, uint64_t seed, long long* counts,
+                 cmc_error* err) {
+  if (G < 1 || N < 1 || L < 1 || !X || !theta || !sigma || !counts) {
+    set_err(err, CMC_ERR_ARG, "bad simulation arguments");
+    return CMC_ERR_ARG;
+  }
+  if (!(nu > 0.0) || !(tau > 0.0)) {
+    set_err(err, CMC_ERR_CONFIG, "nu and tau must be positive");
+    return CMC_ERR_CONFIG;
+  }
+  std::vector<double> beta((size_t)L);
+  for (long g = 0; g < G; ++g) {
+    // beta, gamma, eps draws as P:src/simulate.cpp:51-69
+    Stream rng;
+    rng.init(seed, 0, 0, site_id(kSiteSim, (uint64_t)g));
+    for (long l = 0; l < L; ++l) beta[l] = theta[l] + sigma[l] * normal(rng);
+    const double gam = 1.0 / gamma_draw(rng, nu / 2.0, nu * tau / 2.0);
+    const double sd = std::sqrt(gam);
+    for (long n = 0; n < N; ++n) {
+      const double e = sd * normal(rng);
+      double eta = 0.0;
+      for (long l = 0; l < L; ++l) eta += X[n * L + l] * beta[l];
+      const double arg = (h ? h[n] : 0.0) + e + eta;
+      if (arg > 700.0 || std::exp(arg) > 1e15) {
+        char buf[160];
+        std::snprintf(buf, sizeof(buf),
+                      "simulated Poisson mean overflow at gene %ld, sample %ld", g + 1,
+                      n + 1);
+        set_err(err, CMC_ERR_CONFIG, buf);
+        return CMC_ERR_CONFIG;
+      }
+      counts[g * N + n] = poisson_draw(rng, std::exp(arg));
+    }
+  }
+  return CMC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+// Device-side data layout of the B200 Gibbs sweep and the launch wrappers
+// the host engine (engine.cu) calls.  See DESIGN.md "Data layout in HBM".
+//
+// Gene state is structure-of-arrays, gene index fastest, so adjacent
+// threads (= adjacent genes) touch adjacent 8-byte words:
+//   y[n][g], eps[n][g], eps_w[n][g], eps_wa[n][g], gamma[g], beta[l][g],
+//   A[l][g], accumulators acc_*[4][k][g] (mean, meansq, mean_c, meansq_c).
+// Every per-chain array is repeated with a chain stride; chains are the
+// grid's y dimension.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cmc {
+
+constexpr int kLMax = 16;         // model-matrix columns supported
+constexpr int kLeaf = 1024;       // reference reduction leaf, P:include/countmc/parallel.hpp:60
+constexpr int kGeneBlock = 128;   // threads (= genes) per sweep block
+constexpr int kMaxContrasts = 8;
+constexpr int kMaxTerms = 32;
+constexpr int kMaxCoefs = 64;
+constexpr unsigned long long kNoError = ~0ull;
+
+// Stall key: (step rank 4 bits | column 8 bits | gene 32 bits | sample 20
+// bits) so that the numerically smallest key is the stall the reference's
+// sequential sweep would hit first (steps 1..7 in order, beta column-major
+// over genes, P:src/engine.cpp:178-369).
+__host__ __device__ inline unsigned long long stall_key(unsigned step,
+                                                        unsigned col,
+                                                        unsigned long long g,
+                                                        unsigned n) {
+  return ((unsigned long long)step << 60) | ((unsigned long long)col << 52) |
+         (g << 20) | (unsigned long long)n;
+}
+
+// Hyperparameters, their tuning, monitors and bookkeeping for one chain.
+struct Hyper {
+  double nu, tau;
+  double theta[kLMax];
+  double sigma[kLMax];
+  double w_nu, wa_nu, w_tau, wa_tau;
+  double w_sigma[kLMax];
+  double wa_sigma[kLMax];
+  // Welford monitors [mean, meansq, mean_c, meansq_c] x [nu, tau, theta, sigma]
+  double acc[4][2 + 2 * kLMax];
+  unsigned long long clamps;
+  unsigned long long err_key;
+  double err_x0[2 + kLMax];  // nu, tau, sigma_l
+  double err_w[2 + kLMax];
+  long long err_m;            // iteration of the recorded stall
+  unsigned int doneA, doneB;  // last-block counters of the two leaf phases
+};
+
+struct ContrastTable {
+  int n;
+  int gene_needs_hyper;  // a per-gene contrast reads theta/sigma/nu/tau
+  int per_gene[kMaxContrasts];
+  int term_begin[kMaxContrasts + 1];
+  int coef_begin[kMaxTerms + 1];
+  double threshold[kMaxTerms];
+  int fam[kMaxCoefs];
+  int idx[kMaxCoefs];
+  double coef[kMaxCoefs];
+  long prob_off[kMaxContrasts];
+  long n_prob;  // per chain
+};
+
+struct SweepParams {
+  // problem (this shard)
+  int G;         // local genes
+  int N, L;
+  long g0;       // global index of the first local gene
+  long G_total;  // genes over all shards
+  int n_leaves_local;
+  int n_leaves_total;
+  int leaves_per_rank;  // leaf stride of the gathered partial buffers
+  int world;
+  int Jmax;
+  int fuse_tail;  // single GPU: the last leaf block runs the hyper step
+  const double* y;  // [N][G]
+  const double* A;  // [L][G]
+  const double* X;  // [N*L] row-major
+  const double* h;  // [N]
+  const int* grp_off;   // [L+1]
+  const double* grp_val;
+  const int* grp_moff;  // [n_groups+1]
+  const int* grp_mem;
+  double a, b, d;
+  double c[kLMax], s[kLMax];
+  double exp_clamp;  // exp(700) as the host libm rounds it
+  // config
+  uint64_t seed;
+  int chain_base;  // chain id of grid.y == 0
+  int slot_base;   // state slot of grid.y == 0
+  int K, max_shrink;
+  long burnin, tune_cutoff, thin, n_rows, n_cols, n_saved;
+  int direct;
+  const long* d_m;  // device iteration base; kernels use *d_m + m_off
+  // state, chain stride = element count of one chain
+  double *eps, *eps_w, *eps_wa;
+  double *gam, *gam_w, *gam_wa;
+  double *beta, *beta_w, *beta_wa;
+  double *log_gam, *inv_gam;
+  Hyper* hyper;
+  // monitoring
+  int monitor_enabled;  // run_chain semantics (accumulators/contrasts/thin)
+  double *acc_eps, *acc_gam, *acc_beta;
+  double* cprob;  // [C][n_prob]
+  const ContrastTable* ctab;
+  int ctab_n, ctab_gene_in_sweep;
+  double* samples;  // [C][n_cols][n_rows]
+  const int* saved_slot;  // [G] local: saved index or -1
+  // reductions
+  double* partA;  // [world][C][2+L][leaves_per_rank]
+  double* partB;  // [world][C][L][leaves_per_rank]
+  int C;          // chains resident (stride of the partial buffers)
+  double *stall_x0, *stall_w;  // [C][G]
+};
+
+// Launch wrappers (sweep_kernels.cu).  `chains` = grid.y.
+cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
+                              cudaStream_t s);
+cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
+                          cudaStream_t s);
+cudaError_t launch_hyper_a(const SweepParams& p, int chains, long m_off,
+                           cudaStream_t s);
+cudaError_t launch_leaf_b(const SweepParams& p, int chains, long m_off,
+                          cudaStream_t s);
+cudaError_t launch_hyper_b(const SweepParams& p, int chains, long m_off,
+                           cudaStream_t s);
+cudaError_t launch_gene_contrast(const SweepParams& p, int chains, long m_off,
+                                 cudaStream_t s);
+cudaError_t launch_advance(long* d_m, long by, cudaStream_t s);
+cudaError_t launch_compute_A(const double* y, const double* X, double* A,
+                             int G, int N, int L, cudaStream_t s);
+int gene_sweep_smem_bytes(int N, int Jmax);
+
+}  // namespace cmc

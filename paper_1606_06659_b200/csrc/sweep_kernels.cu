@@ -1,0 +1,892 @@
+// B200 kernels for one Gibbs sweep of the two-level Poisson-lognormal model
+// (reference GibbsEngine::iterate, P:src/engine.cpp:161-370, plus the
+// run_chain monitors, P:src/engine.cpp:409-447).
+//
+// Per iteration m (single GPU, three launches captured in a CUDA graph):
+//   gene_sweep  one thread per gene: eps_g1..eps_gN slice steps (step 1),
+//               gamma_g (step 2), beta_g1..beta_gL (step 5), fused Welford
+//               monitors, per-gene contrasts and thinning of saved genes.
+//               Steps 1, 2 and 5 fuse because beta's full conditional does
+//               not read nu, tau or gamma (P:src/engine.cpp:275-331) and
+//               everything else it needs is the previous iteration's
+//               hyperparameters.
+//   leaf_a      one block per 1024-gene reduction leaf: serial leaf sums of
+//               log gamma, 1/gamma, beta_l (the reference tree,
+//               P:include/countmc/parallel.hpp:67-84); the last block to
+//               finish draws nu, tau (steps 3-4) and theta (step 6).
+//   leaf_b      leaf sums of (beta_l - theta_l)^2; the last block draws
+//               sigma (step 7) and updates the hyper monitors / thinning.
+// Multi-GPU runs the leaf kernels on local leaves, all-gathers the partial
+// sums, and runs hyper_a / hyper_b as separate single-block kernels.
+//
+// Compiled with -fmad=false: every expression below rounds exactly as the
+// reference's non-FMA x86-64 build (P:CMakeLists.txt:7-9), which makes the
+// sampled values bit-identical to the reference for identical uniforms.
+#include <math.h>
+
+#include "rng.cuh"
+#include "sweep.h"
+
+namespace cmc {
+
+namespace {
+
+constexpr double kExpClamp = 700.0;  // P:include/countmc/model.hpp:14
+
+struct SliceCfg {
+  int K;
+  int max_shrink;
+  long burnin;
+  long tune_cutoff;
+};
+
+// P:include/countmc/slice.hpp:27-35
+__device__ __forceinline__ void tune_update(double& w, double& wa, long m,
+                                            double delta, long cutoff) {
+  const double md = (double)m;
+  wa += md * delta;
+  if (m > cutoff) {
+    const double nw = wa / (0.5 * md * (md + 1.0));
+    if (nw >= 1e-12) w = nw;
+  }
+}
+
+// Stepping-out + shrinkage slice step with the reference's draw order
+// (P:include/countmc/slice.hpp:42-75), written as ONE loop that performs
+// one log-density evaluation per trip whatever phase (step-out left,
+// step-out right, shrink) a lane is in: a warp pays the maximum of the
+// lanes' total evaluation counts, not the sum of per-phase maxima.
+template <class F>
+__device__ __forceinline__ double slice_step(F& f, double x0, double& w,
+                                             double& wa, const SliceCfg& sc,
+                                             long m, Stream& rng,
+                                             bool& stalled) {
+  const double fx0 = f(x0);
+  const double logu = fx0 + log(rng.u01());
+  const double wv = w;
+  double lo = x0 - wv * rng.u01();
+  double hi = lo + wv;
+  uint64_t kl = rng.uniform_int((uint64_t)sc.K + 1);
+  uint64_t kr = (uint64_t)sc.K - kl;
+  int phase = kl > 0 ? 0 : (kr > 0 ? 1 : 2);
+  int it = 0;
+  double x1 = x0;
+  for (;;) {
+    double xe;
+    if (phase == 2) {
+      x1 = lo + (hi - lo) * rng.u01();
+      xe = x1;
+    } else {
+      xe = phase == 0 ? lo : hi;
+    }
+    const double fe = f(xe);
+    if (phase == 0) {
+      if (logu < fe) {
+        lo -= wv;
+        if (--kl == 0) phase = kr > 0 ? 1 : 2;
+      } else {
+        phase = kr > 0 ? 1 : 2;
+      }
+    } else if (phase == 1) {
+      if (logu < fe) {
+        hi += wv;
+        if (--kr == 0) phase = 2;
+      } else {
+        phase = 2;
+      }
+    } else {
+      if (fe > logu) break;
+      if (x1 > x0)
+        hi = x1;
+      else
+        lo = x1;
+      if (++it >= sc.max_shrink) {
+        stalled = true;
+        return x0;
+      }
+    }
+  }
+  if (m <= sc.burnin) tune_update(w, wa, m, fabs(x1 - x0), sc.tune_cutoff);
+  return x1;
+}
+
+// log full conditional of eps_gn, P:src/model.cpp:70-74 (clamped_exp
+// :13-19): y*e - exp(min(h + eta + e, 700)) - e*e / (2 gamma).
+struct EpsF {
+  double y, cn, two_gam;
+  unsigned clamps;
+  __device__ __forceinline__ double operator()(double x) {
+    double t = cn + x;
+    if (t > kExpClamp) {
+      ++clamps;
+      t = kExpClamp;
+    }
+    return y * x - exp(t) - x * x / two_gam;
+  }
+};
+
+// log inverse-gamma, P:src/model.cpp:84-87
+struct InvGammaF {
+  double neg_shape1, scale;
+  __device__ __forceinline__ double operator()(double x) const {
+    if (!(x > 0.0)) return -INFINITY;
+    return neg_shape1 * log(x) - scale / x;
+  }
+};
+
+// log gamma with rate, P:src/model.cpp:89-92
+struct GammaRateF {
+  double shape1, rate;
+  __device__ __forceinline__ double operator()(double x) const {
+    if (!(x > 0.0)) return -INFINITY;
+    return shape1 * log(x) - rate * x;
+  }
+};
+
+// P:src/model.cpp:94-100
+struct NuF {
+  double Gd, tau, s1, s2, d;
+  __device__ __forceinline__ double operator()(double nu) const {
+    if (!(nu > 0.0) || !(nu < d)) return -INFINITY;
+    return -Gd * lgamma(nu / 2.0) + (Gd * nu / 2.0) * log(nu * tau / 2.0) -
+           (nu / 2.0) * (s1 + tau * s2);
+  }
+};
+
+// P:src/model.cpp:131-136
+struct SigmaF {
+  double Gd, ss, bound;
+  __device__ __forceinline__ double operator()(double s) const {
+    if (!(s > 0.0) || !(s < bound)) return -INFINITY;
+    return -Gd * log(s) - ss / (2.0 * s * s);
+  }
+};
+
+// Grouped beta density, P:src/engine.cpp:303-316: exp(base + v b) is
+// factored as S_j exp(v_j b) over the distinct nonzero column values.
+struct BetaF {
+  double a, theta, two_sig2, e700;
+  const double* val;   // group values (uniform across the warp)
+  const double* S;     // shared memory, stride kGeneBlock
+  const double* logS;
+  int J;
+  unsigned clamps;
+  __device__ __forceinline__ double operator()(double b) {
+    double tot = a * b;
+    for (int j = 0; j < J; ++j) {
+      const double t = val[j] * b;
+      const double lS = logS[j * kGeneBlock];
+      const double Sj = S[j * kGeneBlock];
+      if (lS + t > kExpClamp) {
+        ++clamps;
+        tot -= e700;
+      } else if (Sj > 0.0) {
+        tot -= Sj * exp(t);
+      }
+    }
+    const double zz = b - theta;
+    return tot - zz * zz / two_sig2;
+  }
+};
+
+// Kahan add, P:include/countmc/streaming.hpp:29-34
+__device__ __forceinline__ void kahan(double& sum, double& comp, double term) {
+  const double y = term - comp;
+  const double t = sum + y;
+  comp = (t - sum) - y;
+  sum = t;
+}
+
+// MomentAccumulator::update on SoA storage acc[k * stride] (k = mean,
+// meansq, mean_c, meansq_c), P:include/countmc/streaming.hpp:17-22.
+__device__ __forceinline__ void moments(double* acc, size_t stride, double v,
+                                        double mcount) {
+  double mean = acc[0], meansq = acc[stride], mc = acc[2 * stride],
+         msc = acc[3 * stride];
+  kahan(mean, mc, (v - mean) / mcount);
+  kahan(meansq, msc, (v * v - meansq) / mcount);
+  acc[0] = mean;
+  acc[stride] = meansq;
+  acc[2 * stride] = mc;
+  acc[3 * stride] = msc;
+}
+
+// Every stall of a chain happens in one iteration (later kernels of a
+// stalled chain return at entry), so err_m is written with one value.
+__device__ __forceinline__ void record_stall(Hyper* hp, unsigned long long key,
+                                             long m) {
+  atomicMin(&hp->err_key, key);
+  hp->err_m = m;
+}
+
+// Accessor for the gathered leaf partials: [rank][C][Q][leaves_per_rank].
+__device__ __forceinline__ double leaf_part(const double* part,
+                                            const SweepParams& p, int slot,
+                                            int Q, int q, long leaf) {
+  const long lpr = p.leaves_per_rank;
+  const long r = leaf / lpr, j = leaf % lpr;
+  return __ldcg(part + (((r * p.C + slot) * Q + q) * lpr + j));
+}
+
+// pairwise_sum over the leaf partials, P:src/parallel.cpp:81-86.
+__device__ __noinline__ double pairwise_leaves(const double* part,
+                                               const SweepParams& p, int slot,
+                                               int Q, int q, long lo, long n) {
+  if (n == 0) return 0.0;
+  if (n == 1) return leaf_part(part, p, slot, Q, q, lo);
+  const long mid = n / 2;
+  return pairwise_leaves(part, p, slot, Q, q, lo, mid) +
+         pairwise_leaves(part, p, slot, Q, q, lo + mid, n - mid);
+}
+
+__device__ double param_value(const ContrastTable* t, int k, const double* beta,
+                              size_t G, long gl, double gam, const Hyper* hp) {
+  const int fam = t->fam[k], idx = t->idx[k];
+  switch (fam) {
+    case 0: return beta[(size_t)idx * G + gl];
+    case 1: return gam;
+    case 2: return hp->theta[idx];
+    case 3: return hp->sigma[idx];
+    case 4: return hp->nu;
+    default: return hp->tau;
+  }
+}
+
+// ContrastAccumulator::update for one slot, P:src/streaming.cpp:90-108.
+__device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
+                                double mcount, const double* beta, size_t G,
+                                long gl, double gam, const Hyper* hp) {
+  bool all = true;
+  for (int term = t->term_begin[ci]; term < t->term_begin[ci + 1]; ++term) {
+    double lhs = 0.0;
+    for (int k = t->coef_begin[term]; k < t->coef_begin[term + 1]; ++k)
+      lhs += t->coef[k] * param_value(t, k, beta, G, gl, gam, hp);
+    if (!(lhs > t->threshold[term])) {
+      all = false;
+      break;
+    }
+  }
+  const double ind = all ? 1.0 : 0.0;
+  *prob += (ind - *prob) / mcount;
+}
+
+// ---------------------------------------------------------------- kernels
+
+// One thread per gene.  Lanes of a warp are re-converged with __syncwarp()
+// at every slice-step boundary so each step's log-density evaluations run
+// as one SIMT stream (no early exits: a lane without a gene, or whose gene
+// stalled, idles with alive == false).
+__global__ void __launch_bounds__(kGeneBlock)
+    gene_sweep_kernel(const SweepParams p, const long m_off) {
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x;
+  const int slot = p.slot_base + blockIdx.y;
+  Hyper* hp = p.hyper + slot;
+  if (hp->err_key != kNoError) return;  // warp-uniform: one load per warp
+  const long gl_raw = (long)blockIdx.x * kGeneBlock + tid;
+  bool alive = gl_raw < p.G;
+  const long gl = alive ? gl_raw : 0;
+
+  const long m = *p.d_m + m_off;
+  const bool tuning = m <= p.burnin;
+  const bool monitor = p.monitor_enabled && m > p.burnin;
+  const double mcount = (double)(m - p.burnin);
+  const int N = p.N, L = p.L;
+  const size_t G = (size_t)p.G;
+  const uint64_t chain = (uint64_t)(p.chain_base + blockIdx.y);
+  const uint64_t gg = (uint64_t)(p.g0 + gl);
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff};
+  const size_t so = (size_t)slot;
+
+  double* eps = p.eps + so * N * G;
+  double* eps_w = p.eps_w + so * N * G;
+  double* eps_wa = p.eps_wa + so * N * G;
+  double* beta = p.beta + so * L * G;
+  double* beta_w = p.beta_w + so * L * G;
+  double* beta_wa = p.beta_wa + so * L * G;
+  double* xs = smem;                             // [N][B]: xb, then lp
+  double* sS = smem + (size_t)N * kGeneBlock;    // [Jmax][B]
+  double* sLogS = sS + (size_t)p.Jmax * kGeneBlock;
+  unsigned clamps = 0;
+
+  // refresh_xb, P:src/engine.cpp:144-159 (l ascending from 0.0 per n)
+  for (int n = 0; n < N; ++n) xs[n * kGeneBlock + tid] = 0.0;
+  for (int l = 0; l < L; ++l) {
+    const double b = alive ? beta[(size_t)l * G + gl] : 0.0;
+    for (int n = 0; n < N; ++n)
+      xs[n * kGeneBlock + tid] += __ldg(p.X + n * L + l) * b;
+  }
+
+  // Step 1: eps_gn, P:src/engine.cpp:178-202
+  const double gam_old = alive ? p.gam[so * G + gl] : 1.0;
+  const double two_gam = 2.0 * gam_old;
+  double ss = 0.0;
+  for (int n = 0; n < N; ++n) {
+    __syncwarp();
+    if (!alive) continue;
+    const size_t i = (size_t)n * G + gl;
+    const double hn = __ldg(p.h + n);
+    EpsF f{__ldg(p.y + i), hn + xs[n * kGeneBlock + tid], two_gam, 0u};
+    const double x0 = eps[i];
+    const double w0 = eps_w[i];
+    double w = w0, wa = tuning ? eps_wa[i] : 0.0;
+    Stream rng;
+    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
+    bool st = false;
+    const double x1 = slice_step(f, x0, w, wa, sc, m, rng, st);
+    clamps += f.clamps;
+    if (st) {
+      p.stall_x0[so * G + gl] = x0;
+      p.stall_w[so * G + gl] = w0;
+      record_stall(hp, stall_key(1, 0, gg, n), m);
+      alive = false;
+      continue;
+    }
+    eps[i] = x1;
+    if (tuning) {
+      eps_w[i] = w;
+      eps_wa[i] = wa;
+    }
+    ss += x1 * x1;
+    xs[n * kGeneBlock + tid] = hn + x1 + xs[n * kGeneBlock + tid];  // lp
+    if (monitor) moments(p.acc_eps + so * 4 * N * G + i, (size_t)N * G, x1, mcount);
+  }
+
+  // Step 2: gamma_g, P:src/engine.cpp:204-226 (nu, tau of iteration m-1)
+  __syncwarp();
+  if (alive) {
+    const double nu = hp->nu, tau = hp->tau;
+    const double shape = (nu + (double)N) / 2.0;
+    const double scale = (nu * tau + ss) / 2.0;
+    Stream rng;
+    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteGamma, gg));
+    double gnew = gam_old;
+    if (p.direct) {
+      gnew = 1.0 / gamma_draw(rng, shape, scale);
+    } else {
+      InvGammaF f{-(shape + 1.0), scale};
+      const double w0 = p.gam_w[so * G + gl];
+      double w = w0, wa = tuning ? p.gam_wa[so * G + gl] : 0.0;
+      bool st = false;
+      gnew = slice_step(f, gam_old, w, wa, sc, m, rng, st);
+      if (st) {
+        p.stall_x0[so * G + gl] = gam_old;
+        p.stall_w[so * G + gl] = w0;
+        record_stall(hp, stall_key(2, 0, gg, 0), m);
+        alive = false;
+      } else if (tuning) {
+        p.gam_w[so * G + gl] = w;
+        p.gam_wa[so * G + gl] = wa;
+      }
+    }
+    if (alive) {
+      p.gam[so * G + gl] = gnew;
+      p.log_gam[so * G + gl] = log(gnew);
+      p.inv_gam[so * G + gl] = 1.0 / gnew;
+      if (monitor) moments(p.acc_gam + so * 4 * G + gl, G, gnew, mcount);
+    }
+  }
+
+  // Step 5: beta_g1..beta_gL in column order, P:src/engine.cpp:269-334
+  for (int l = 0; l < L; ++l) {
+    __syncwarp();
+    if (!alive) continue;
+    const size_t i = (size_t)l * G + gl;
+    const double bold = beta[i];
+    const int jb = __ldg(p.grp_off + l), je = __ldg(p.grp_off + l + 1);
+    for (int j = jb; j < je; ++j) {
+      const double v = __ldg(p.grp_val + j);
+      double s = 0.0;
+      for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
+        const int n = __ldg(p.grp_mem + q);
+        double t = xs[n * kGeneBlock + tid] - v * bold;
+        if (t > kExpClamp) {
+          ++clamps;
+          t = kExpClamp;
+        }
+        s += exp(t);
+      }
+      sS[(j - jb) * kGeneBlock + tid] = s;
+      sLogS[(j - jb) * kGeneBlock + tid] = log(s);
+    }
+    const double sig = hp->sigma[l];
+    const double sig2 = sig * sig;
+    BetaF f{__ldg(p.A + i), hp->theta[l], 2.0 * sig2, p.exp_clamp,
+            p.grp_val + jb, sS + tid, sLogS + tid, je - jb, 0u};
+    const double w0 = beta_w[i];
+    double w = w0, wa = tuning ? beta_wa[i] : 0.0;
+    Stream rng;
+    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l));
+    bool st = false;
+    const double bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
+    clamps += f.clamps;
+    if (st) {
+      p.stall_x0[so * G + gl] = bold;
+      p.stall_w[so * G + gl] = w0;
+      record_stall(hp, stall_key(5, l, gg, 0), m);
+      alive = false;
+      continue;
+    }
+    beta[i] = bnew;
+    if (tuning) {
+      beta_w[i] = w;
+      beta_wa[i] = wa;
+    }
+    if (bnew != bold) {
+      for (int j = jb; j < je; ++j) {
+        const double v = __ldg(p.grp_val + j);
+        for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
+          const int n = __ldg(p.grp_mem + q);
+          xs[n * kGeneBlock + tid] += v * (bnew - bold);
+        }
+      }
+    }
+    if (monitor) moments(p.acc_beta + so * 4 * L * G + i, (size_t)L * G, bnew, mcount);
+  }
+
+  __syncwarp();
+  if (alive && monitor) {
+    // per-gene contrasts that read only this gene's beta/gamma
+    if (p.ctab_gene_in_sweep) {
+      const ContrastTable* t = p.ctab;
+      const double gam = p.gam[so * G + gl];
+      for (int ci = 0; ci < p.ctab_n; ++ci)
+        if (t->per_gene[ci])
+          contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + gl,
+                          mcount, beta, G, gl, gam, hp);
+    }
+    // thinning of saved genes, P:src/engine.cpp:433-447
+    const long cnt = m - p.burnin;
+    const int sv = p.saved_slot[gl];
+    if (sv >= 0 && cnt % p.thin == 0) {
+      const long row = cnt / p.thin - 1;
+      if (row < p.n_rows) {
+        double* smp = p.samples + so * p.n_cols * p.n_rows;
+        const long c0 = 2 + 2 * (long)L + (long)sv * (L + 1);
+        for (int l = 0; l < L; ++l)
+          smp[(c0 + l) * p.n_rows + row] = beta[(size_t)l * G + gl];
+        smp[(c0 + L) * p.n_rows + row] = p.gam[so * G + gl];
+      }
+    }
+  }
+  if (clamps) atomicAdd(&hp->clamps, (unsigned long long)clamps);
+}
+
+// Serial sum of one 1024-gene leaf by one warp, in gene order: every lane
+// carries the same running sum; the leaf's 1024 values are loaded up front
+// (32 independent coalesced loads per lane) and broadcast lane by lane, so
+// the only dependent chain is the reference's left-to-right leaf loop
+// (P:include/countmc/parallel.hpp:76-81).
+template <class V>
+__device__ __forceinline__ double warp_leaf_sum(V value, long start, long end) {
+  const int lane = threadIdx.x & 31;
+  const long n = end - start;
+  double v[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const long idx = start + c * 32 + lane;
+    v[c] = idx < end ? value(idx) : 0.0;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double vj = __shfl_sync(0xffffffffu, v[c], j);
+      if (c * 32 + j < n) s += vj;
+    }
+  }
+  return s;
+}
+
+__device__ __noinline__ double pairwise_rec(const double* x, int n) {
+  if (n == 0) return 0.0;
+  if (n == 1) return x[0];
+  const int mid = n / 2;
+  return pairwise_rec(x, mid) + pairwise_rec(x + mid, n - mid);
+}
+
+// pairwise_sum (P:src/parallel.cpp:81-86) of one quantity's leaf partials
+// by one warp.  Lane k walks the top five midpoint splits along the bits of
+// k, sums its depth-5 subtree serially with the same recursion, and the 31
+// internal nodes above are rebuilt with shuffles as left + right.  A node of
+// size 1 passes its single leaf through and a node of size 0 is 0.0, as the
+// reference recursion returns them, so the result is bit-identical.
+__device__ double warp_pairwise_leaves(const double* part, const SweepParams& p,
+                                       int slot, int Q, int q, int n) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, cnt = n;
+  int cnts[5];
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    cnts[d] = cnt;
+    const int mid = cnt / 2;
+    if ((lane >> (4 - d)) & 1) {
+      lo += mid;
+      cnt -= mid;
+    } else {
+      cnt = mid;
+    }
+  }
+  double v;
+  if (cnt <= 64) {
+    double buf[64];
+    for (int i = 0; i < cnt; ++i) buf[i] = leaf_part(part, p, slot, Q, q, lo + i);
+    v = pairwise_rec(buf, cnt);
+  } else {
+    v = pairwise_leaves(part, p, slot, Q, q, lo, cnt);
+  }
+#pragma unroll
+  for (int d = 4; d >= 0; --d) {
+    const int bit = 4 - d;
+    const double other = __shfl_xor_sync(0xffffffffu, v, 1 << bit);
+    const bool right = (lane >> bit) & 1;
+    if (cnts[d] == 0)
+      v = 0.0;
+    else if (cnts[d] == 1)
+      v = right ? v : other;
+    else
+      v = right ? (other + v) : (v + other);
+  }
+  return v;
+}
+
+// Steps 3, 4 and 6: nu, tau and theta from the gathered leaf sums.  Called
+// by a whole block of 32*(2+L) threads (warp q reduces quantity q).
+__device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
+  __shared__ double red[2 + kLMax];
+  Hyper* hp = p.hyper + slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint64_t chain = (uint64_t)(p.chain_base + (slot - p.slot_base));
+  const int L = p.L, Q = 2 + L;
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff};
+  const double Gd = (double)p.G_total;
+  if (warp < Q) {
+    const double r = warp_pairwise_leaves(p.partA, p, slot, Q, warp, p.n_leaves_total);
+    if ((tid & 31) == 0) red[warp] = r;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const double s1 = red[0], s2 = red[1];
+    // Step 3: nu, P:src/engine.cpp:228-248
+    {
+      NuF f{Gd, hp->tau, s1, s2, p.d};
+      Stream rng;
+      rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteNu, 0));
+      double w = hp->w_nu, wa = hp->wa_nu;
+      bool st = false;
+      const double x0 = hp->nu;
+      const double v = slice_step(f, x0, w, wa, sc, m, rng, st);
+      if (st) {
+        hp->err_x0[0] = x0;
+        hp->err_w[0] = hp->w_nu;
+        record_stall(hp, stall_key(3, 0, 0, 0), m);
+        return;
+      }
+      hp->nu = v;
+      hp->w_nu = w;
+      hp->wa_nu = wa;
+    }
+    // Step 4: tau, P:src/engine.cpp:250-267 / P:src/model.cpp:102-105
+    {
+      const double nu = hp->nu;
+      const double shape = p.a + Gd * nu / 2.0;
+      const double rate = p.b + (nu / 2.0) * s2;
+      Stream rng;
+      rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteTau, 0));
+      if (p.direct) {
+        hp->tau = gamma_draw(rng, shape, rate);
+      } else {
+        GammaRateF f{shape - 1.0, rate};
+        double w = hp->w_tau, wa = hp->wa_tau;
+        bool st = false;
+        const double x0 = hp->tau;
+        const double v = slice_step(f, x0, w, wa, sc, m, rng, st);
+        if (st) {
+          hp->err_x0[1] = x0;
+          hp->err_w[1] = hp->w_tau;
+          record_stall(hp, stall_key(4, 0, 0, 0), m);
+          return;
+        }
+        hp->tau = v;
+        hp->w_tau = w;
+        hp->wa_tau = wa;
+      }
+    }
+  } else if (tid >= 32 && tid < 32 + L) {
+    // Step 6: theta_l, P:src/engine.cpp:336-347 / P:src/model.cpp:124-129
+    const int l = tid - 32;
+    const double sb = red[2 + l];
+    const double sg = hp->sigma[l], c = p.c[l];
+    const double v = 1.0 / (1.0 / (c * c) + Gd / (sg * sg));
+    const double mean = v * sb / (sg * sg);
+    const double sd = sqrt(v);
+    Stream rng;
+    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteTheta, l));
+    hp->theta[l] = mean + sd * normal(rng);
+  }
+}
+
+// Step 7 plus the hyper monitors, global contrasts and thinning.
+__device__ void hyper_b_body(const SweepParams& p, int slot, long m) {
+  __shared__ double red[kLMax];
+  Hyper* hp = p.hyper + slot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint64_t chain = (uint64_t)(p.chain_base + (slot - p.slot_base));
+  const int L = p.L;
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff};
+  if (warp < L) {
+    const double r = warp_pairwise_leaves(p.partB, p, slot, L, warp, p.n_leaves_total);
+    if ((tid & 31) == 0) red[warp] = r;
+  }
+  __syncthreads();
+  if (tid < L) {
+    // Step 7: sigma_l, P:src/engine.cpp:349-369
+    const int l = tid;
+    const double ss = red[l];
+    SigmaF f{(double)p.G_total, ss, p.s[l]};
+    Stream rng;
+    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteSigma, l));
+    double w = hp->w_sigma[l], wa = hp->wa_sigma[l];
+    bool st = false;
+    const double x0 = hp->sigma[l];
+    const double v = slice_step(f, x0, w, wa, sc, m, rng, st);
+    if (st) {
+      hp->err_x0[2 + l] = x0;
+      hp->err_w[2 + l] = hp->w_sigma[l];
+      record_stall(hp, stall_key(7, l, 0, 0), m);
+    } else {
+      hp->sigma[l] = v;
+      hp->w_sigma[l] = w;
+      hp->wa_sigma[l] = wa;
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && p.monitor_enabled && m > p.burnin &&
+      hp->err_key == kNoError) {
+    const long cnt = m - p.burnin;
+    const double mc = (double)cnt;
+    const int K = 2 + 2 * kLMax;
+    auto upd = [&](int k, double v) {
+      double mean = hp->acc[0][k], meansq = hp->acc[1][k], c1 = hp->acc[2][k],
+             c2 = hp->acc[3][k];
+      kahan(mean, c1, (v - mean) / mc);
+      kahan(meansq, c2, (v * v - meansq) / mc);
+      hp->acc[0][k] = mean;
+      hp->acc[1][k] = meansq;
+      hp->acc[2][k] = c1;
+      hp->acc[3][k] = c2;
+    };
+    (void)K;
+    upd(0, hp->nu);
+    upd(1, hp->tau);
+    for (int l = 0; l < L; ++l) upd(2 + l, hp->theta[l]);
+    for (int l = 0; l < L; ++l) upd(2 + L + l, hp->sigma[l]);
+    const ContrastTable* t = p.ctab;
+    for (int ci = 0; ci < p.ctab_n; ++ci)
+      if (!t->per_gene[ci])
+        contrast_update(t, ci, p.cprob + (size_t)slot * t->n_prob + t->prob_off[ci],
+                        mc, nullptr, 0, 0, 0.0, hp);
+    if (cnt % p.thin == 0) {
+      const long row = cnt / p.thin - 1;
+      if (row < p.n_rows) {
+        double* smp = p.samples + (size_t)slot * p.n_cols * p.n_rows;
+        long col = 0;
+        smp[(col++) * p.n_rows + row] = hp->nu;
+        smp[(col++) * p.n_rows + row] = hp->tau;
+        for (int l = 0; l < L; ++l) smp[(col++) * p.n_rows + row] = hp->theta[l];
+        for (int l = 0; l < L; ++l) smp[(col++) * p.n_rows + row] = hp->sigma[l];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool last_block(unsigned int* counter, unsigned total) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(counter, 1u);
+    is_last = (prev == total - 1);
+    if (is_last) *counter = 0;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// Leaf sums of log gamma (q=0), 1/gamma (q=1), beta_l (q=2+l); one warp
+// per quantity, one block per local leaf.
+__global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
+  const int slot = p.slot_base + blockIdx.y;
+  Hyper* hp = p.hyper + slot;
+  if (hp->err_key != kNoError) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = p.L, Q = 2 + L;
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const long lb = blockIdx.x;
+  const long start = lb * kLeaf;
+  const long end = min((long)G, start + kLeaf);
+  if (warp < Q) {
+    const double* src = warp == 0   ? p.log_gam + so * G
+                        : warp == 1 ? p.inv_gam + so * G
+                                    : p.beta + so * L * G + (size_t)(warp - 2) * G;
+    const double s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
+    if (lane == 0) {
+      const long lpr = p.leaves_per_rank;
+      const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
+      p.partA[((rank * p.C + slot) * Q + warp) * lpr + lb] = s;
+    }
+  }
+  if (!p.fuse_tail) return;
+  if (!last_block(&hp->doneA, (unsigned)p.n_leaves_local)) return;
+  hyper_a_body(p, slot, *p.d_m + m_off);
+}
+
+__global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
+  const int slot = p.slot_base + blockIdx.x;
+  if (p.hyper[slot].err_key != kNoError) return;
+  hyper_a_body(p, slot, *p.d_m + m_off);
+}
+
+// Leaf sums of (beta_l - theta_l)^2 with theta of this iteration.
+__global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
+  const int slot = p.slot_base + blockIdx.y;
+  Hyper* hp = p.hyper + slot;
+  if (hp->err_key != kNoError) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = p.L;
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const long lb = blockIdx.x;
+  const long start = lb * kLeaf;
+  const long end = min((long)G, start + kLeaf);
+  if (warp < L) {
+    const double th = hp->theta[warp];
+    const double* src = p.beta + so * L * G + (size_t)warp * G;
+    const double s = warp_leaf_sum(
+        [&](long i) {
+          const double dl = src[i] - th;
+          return dl * dl;
+        },
+        start, end);
+    if (lane == 0) {
+      const long lpr = p.leaves_per_rank;
+      const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
+      p.partB[((rank * p.C + slot) * L + warp) * lpr + lb] = s;
+    }
+  }
+  if (!p.fuse_tail) return;
+  if (!last_block(&hp->doneB, (unsigned)p.n_leaves_local)) return;
+  hyper_b_body(p, slot, *p.d_m + m_off);
+}
+
+__global__ void hyper_b_kernel(const SweepParams p, const long m_off) {
+  const int slot = p.slot_base + blockIdx.x;
+  if (p.hyper[slot].err_key != kNoError) return;
+  hyper_b_body(p, slot, *p.d_m + m_off);
+}
+
+// Per-gene contrasts that read hyperparameters of the same iteration: run
+// after hyper_b (only built when such a contrast exists).
+__global__ void gene_contrast_kernel(const SweepParams p, const long m_off) {
+  const int slot = p.slot_base + blockIdx.y;
+  const Hyper* hp = p.hyper + slot;
+  if (hp->err_key != kNoError) return;
+  const long gl = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gl >= p.G) return;
+  const long m = *p.d_m + m_off;
+  if (!(p.monitor_enabled && m > p.burnin)) return;
+  const double mc = (double)(m - p.burnin);
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const ContrastTable* t = p.ctab;
+  const double* beta = p.beta + so * p.L * G;
+  const double gam = p.gam[so * G + gl];
+  for (int ci = 0; ci < p.ctab_n; ++ci)
+    if (t->per_gene[ci])
+      contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + gl, mc,
+                      beta, G, gl, gam, hp);
+}
+
+__global__ void advance_kernel(long* d_m, long by) { *d_m += by; }
+
+// A_gl = sum_n y_gn X_nl accumulated in n order, P:src/engine.cpp:55-60.
+__global__ void compute_A_kernel(const double* y, const double* X, double* A,
+                                 int G, int N, int L) {
+  const long g = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  for (int l = 0; l < L; ++l) {
+    double acc = 0.0;
+    for (int n = 0; n < N; ++n) acc += y[(size_t)n * G + g] * X[n * L + l];
+    A[(size_t)l * G + g] = acc;
+  }
+}
+
+}  // namespace
+
+int gene_sweep_smem_bytes(int N, int Jmax) {
+  return (int)(sizeof(double) * (size_t)(N + 2 * Jmax) * kGeneBlock);
+}
+
+cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
+                              cudaStream_t s) {
+  const int smem = gene_sweep_smem_bytes(p.N, p.Jmax);
+  static int configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(
+        gene_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)chains);
+  gene_sweep_kernel<<<grid, kGeneBlock, smem, s>>>(p, m_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
+                          cudaStream_t s) {
+  const int Q = 2 + p.L;
+  const int threads = 32 * (Q > 2 ? Q : 2);
+  dim3 grid((unsigned)p.n_leaves_local, (unsigned)chains);
+  leaf_a_kernel<<<grid, threads < 64 ? 64 : threads, 0, s>>>(p, m_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hyper_a(const SweepParams& p, int chains, long m_off,
+                           cudaStream_t s) {
+  hyper_a_kernel<<<chains, 32 * (2 + p.L), 0, s>>>(p, m_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_leaf_b(const SweepParams& p, int chains, long m_off,
+                          cudaStream_t s) {
+  const int threads = 32 * (p.L > 1 ? p.L : 1);
+  dim3 grid((unsigned)p.n_leaves_local, (unsigned)chains);
+  leaf_b_kernel<<<grid, threads < 32 ? 32 : threads, 0, s>>>(p, m_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hyper_b(const SweepParams& p, int chains, long m_off,
+                           cudaStream_t s) {
+  hyper_b_kernel<<<chains, 32 * p.L, 0, s>>>(p, m_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gene_contrast(const SweepParams& p, int chains, long m_off,
+                                 cudaStream_t s) {
+  dim3 grid((unsigned)((p.G + 255) / 256), (unsigned)chains);
+  gene_contrast_kernel<<<grid, 256, 0, s>>>(p, m_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_advance(long* d_m, long by, cudaStream_t s) {
+  advance_kernel<<<1, 1, 0, s>>>(d_m, by);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compute_A(const double* y, const double* X, double* A,
+                             int G, int N, int L, cudaStream_t s) {
+  compute_A_kernel<<<(G + 255) / 256, 256, 0, s>>>(y, X, A, G, N, L);
+  return cudaGetLastError();
+}
+
+}  // namespace cmc

@@ -1,0 +1,567 @@
+"""Host-side mirror of the reference countmc engine API over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference headers
+(P: = /root/reference/proj/):
+
+* ``RunConfig`` / ``SliceConfig``    P:include/countmc/engine.hpp:21-36, slice.hpp:11-17
+* ``ChainState``                     P:include/countmc/types.hpp:86-108
+* ``TuningState``                    P:include/countmc/engine.hpp:58-74
+* ``ChainOutput``                    P:include/countmc/engine.hpp:90-108
+* ``GibbsEngine``                    P:include/countmc/engine.hpp:110-159
+* ``ConfigError``/``SamplerStallError`` P:include/countmc/errors.hpp:10-71
+
+Every sweep runs in the CUDA library (``lib/libcountmc_b200.so``); this
+module only marshals arrays.  The library is required: nothing here computes
+a sweep on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_long, c_uint64, c_void_p
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import (CmcError, CmcOutputView, ContrastArrays, ProblemArrays, dptr,
+                   load_library, lptr, sizes)
+
+
+class ConfigError(ValueError):
+    """Bad configuration or inputs (reference ConfigError, exit code 1)."""
+
+
+class SamplerStallError(RuntimeError):
+    """Slice shrink loop exceeded max_shrink (reference SamplerStallError)."""
+
+    def __init__(self, msg, step="", index1=-1, index2=-1, x0=0.0, width=0.0,
+                 iteration=0):
+        super().__init__(msg)
+        self.step = step
+        self.index1 = index1
+        self.index2 = index2
+        self.x0 = x0
+        self.width = width
+        self.iteration = iteration
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL failure inside the library."""
+
+
+def _raise(rc: int, err: CmcError):
+    if rc == _abi.CMC_OK:
+        return
+    msg = err.msg.decode(errors="replace")
+    if rc == _abi.CMC_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == _abi.CMC_ERR_STALL:
+        raise SamplerStallError(msg, err.step.decode(), err.index1, err.index2,
+                                err.x0, err.width, err.iteration)
+    if rc == _abi.CMC_ERR_ARG:
+        raise ValueError(msg)
+    raise DeviceError(msg)
+
+
+@dataclass
+class SliceConfig:
+    max_step_out: int = 100
+    burnin: int = 0
+    tune_cutoff: int = 0
+    w_init: float = 1.0
+    max_shrink: int = 1000
+
+
+@dataclass
+class RunConfig:
+    chains: int = 4
+    iterations: int = 4000
+    burnin: int = 2000
+    tune_cutoff: int = -1
+    thin: int = 20
+    seed: int = 1
+    slice: SliceConfig = field(default_factory=SliceConfig)
+    save_genes: int = 20
+    workers: int = 1
+    sampler_mode: str = "slice_faithful"  # or "conjugate_direct"
+    concurrent_chains: bool = False
+
+    def to_c(self) -> _abi.CmcRunConfig:
+        mode = {"slice_faithful": 0, "conjugate_direct": 1}[self.sampler_mode]
+        return _abi.make_config(self.chains, self.iterations, self.burnin,
+                                self.tune_cutoff, self.thin, self.seed,
+                                self.slice.max_step_out, self.slice.max_shrink,
+                                self.slice.w_init, self.save_genes, self.workers,
+                                mode, self.concurrent_chains)
+
+
+@dataclass
+class PriorConfig:
+    a: float = 1.0
+    b: float = 1.0
+    d: float = 1000.0
+    c: Optional[Sequence[float]] = None  # prior sd of theta_l, default 10
+    s: Optional[Sequence[float]] = None  # upper bound of sigma_l, default 100
+
+    def resolve(self, L: int):
+        """PriorConfig::resolve, P:src/types.cpp:38-43."""
+        if not self.c:
+            self.c = [10.0] * L
+        if not self.s:
+            self.s = [100.0] * L
+        if len(self.c) == 1 and L > 1:
+            self.c = [self.c[0]] * L
+        if len(self.s) == 1 and L > 1:
+            self.s = [self.s[0]] * L
+        return self
+
+
+@dataclass
+class ModelSpec:
+    X: np.ndarray  # N x L
+    h: np.ndarray  # N
+    priors: PriorConfig = field(default_factory=PriorConfig)
+
+    @property
+    def N(self):
+        return self.X.shape[0]
+
+    @property
+    def L(self):
+        return self.X.shape[1]
+
+
+@dataclass
+class CountMatrix:
+    counts: np.ndarray  # G x N int64
+
+    @property
+    def G(self):
+        return self.counts.shape[0]
+
+    @property
+    def N(self):
+        return self.counts.shape[1]
+
+
+class ChainState:
+    """One iteration's parameter values (reference ChainState)."""
+
+    def __init__(self, G, N, L):
+        self.G, self.N, self.L = G, N, L
+        self.eps = np.zeros((G, N))
+        self.gamma = np.ones(G)
+        self.beta = np.zeros((G, L))
+        self.theta = np.zeros(L)
+        self.sigma = np.ones(L)
+        self.nu = 2.0
+        self.tau = 1.0
+
+    def pack(self) -> np.ndarray:
+        return np.concatenate([self.eps.ravel(), self.gamma, self.beta.ravel(),
+                               self.theta, self.sigma, [self.nu, self.tau]]).astype(np.float64)
+
+    @classmethod
+    def unpack(cls, packed, G, N, L) -> "ChainState":
+        st = cls(G, N, L)
+        st.load(packed)
+        return st
+
+    def load(self, p):
+        G, N, L = self.G, self.N, self.L
+        o = 0
+        self.eps = np.array(p[o:o + G * N]).reshape(G, N); o += G * N
+        self.gamma = np.array(p[o:o + G]); o += G
+        self.beta = np.array(p[o:o + G * L]).reshape(G, L); o += G * L
+        self.theta = np.array(p[o:o + L]); o += L
+        self.sigma = np.array(p[o:o + L]); o += L
+        self.nu = float(p[o]); self.tau = float(p[o + 1])
+
+    def check(self, priors: PriorConfig):
+        """ChainState::check, P:src/types.cpp:71-89."""
+        if not np.all(np.isfinite(self.eps)):
+            raise ConfigError("non-finite eps in chain state")
+        if not (np.all(self.gamma > 0) and np.all(np.isfinite(self.gamma))):
+            raise ConfigError("gamma must be positive and finite")
+        if not np.all(np.isfinite(self.beta)):
+            raise ConfigError("non-finite beta in chain state")
+        if not np.all(np.isfinite(self.theta)):
+            raise ConfigError("non-finite theta in chain state")
+        for l in range(self.L):
+            bound = priors.s[l] if l < len(priors.s) else 100.0
+            if not (0.0 < self.sigma[l] < bound):
+                raise ConfigError(f"sigma[{l + 1}] outside (0, s)")
+        if not (0.0 < self.nu < priors.d):
+            raise ConfigError("nu outside (0, d)")
+        if not (self.tau > 0.0 and np.isfinite(self.tau)):
+            raise ConfigError("tau must be positive and finite")
+
+
+class TuningState:
+    """Slice widths w and w_aux in the packed order [eps|gamma|beta|sigma|nu|tau]."""
+
+    def __init__(self, G, N, L, w_init=1.0):
+        _, T, _ = sizes(G, N, L)
+        self.G, self.N, self.L = G, N, L
+        self.w = np.full(T, float(w_init))
+        self.w_aux = np.zeros(T)
+
+    def _slice(self, which):
+        G, N, L = self.G, self.N, self.L
+        o = {"eps": (0, G * N), "gamma": (G * N, G), "beta": (G * N + G, G * L),
+             "sigma": (G * N + G + G * L, L), "nu": (G * N + G + G * L + L, 1),
+             "tau": (G * N + G + G * L + L + 1, 1)}[which]
+        return slice(o[0], o[0] + o[1])
+
+    def width(self, which):
+        return self.w[self._slice(which)]
+
+    def aux(self, which):
+        return self.w_aux[self._slice(which)]
+
+
+class Moments:
+    """Vector of MomentAccumulator (P:include/countmc/streaming.hpp:15-40)."""
+
+    def __init__(self, count, mean, meansq, mean_c, meansq_c):
+        self.count = count
+        self.mean = mean
+        self.meansq = meansq
+        self.mean_c = mean_c
+        self.meansq_c = meansq_c
+
+
+@dataclass
+class ContrastResult:
+    spec: object
+    count: int
+    prob: np.ndarray
+
+
+@dataclass
+class ChainOutput:
+    chain: int
+    nu_acc: Moments
+    tau_acc: Moments
+    theta_acc: Moments
+    sigma_acc: Moments
+    beta_acc: Moments   # arrays G x L
+    gamma_acc: Moments  # G
+    eps_acc: Moments    # G x N
+    contrasts: List[ContrastResult]
+    sample_names: List[str]
+    samples: np.ndarray  # [column][row]
+    sample_iters: np.ndarray
+    saved_genes: np.ndarray
+    step_seconds: np.ndarray
+    clamp_events: int
+    final_state: ChainState
+
+
+# ----------------------------------------------------------------- contrasts
+
+@dataclass
+class ParamRef:
+    family: str  # beta_col, gamma, theta, sigma, nu, tau
+    index: int = 0  # 0-based column
+
+    def per_gene(self):
+        return self.family in ("beta_col", "gamma")
+
+
+def parse_param_ref(name: str, L: int) -> ParamRef:
+    """parse_param_ref, P:src/streaming.cpp:42-74."""
+    bad = ConfigError(f"unknown parameter name in contrast: '{name}'")
+    if name in ("nu", "tau", "gamma"):
+        return ParamRef(name if name != "gamma" else "gamma", 0)
+    if "[" not in name or not name.endswith("]"):
+        raise bad
+    head, inner = name[:name.index("[")], name[name.index("[") + 1:-1]
+    if head == "beta":
+        if len(inner) < 2 or inner[0] != "," or not inner[1:].isdigit():
+            raise bad
+        fam, idx = "beta_col", int(inner[1:])
+    elif head in ("theta", "sigma"):
+        if not inner.isdigit():
+            raise bad
+        fam, idx = head, int(inner)
+    elif head == "gamma":
+        raise ConfigError("gamma takes no index in contrasts; write 'gamma'")
+    else:
+        raise bad
+    if idx < 1 or idx > L:
+        raise ConfigError(f"contrast index out of range in '{name}' (L={L})")
+    return ParamRef(fam, idx - 1)
+
+
+@dataclass
+class ContrastTerm:
+    coeffs: List[tuple]  # [(ParamRef, coef)]
+    threshold: float = 0.0
+
+
+@dataclass
+class ContrastSpec:
+    id: str
+    terms: List[ContrastTerm]
+    per_gene: bool = False
+
+    def finalize(self):
+        """ContrastSpec::finalize, P:src/streaming.cpp:76-88."""
+        if not self.terms:
+            raise ConfigError(f"contrast '{self.id}' has no terms")
+        self.per_gene = False
+        for t in self.terms:
+            if not t.coeffs:
+                raise ConfigError(f"contrast '{self.id}' has a term with no coefficients")
+            for ref, _ in t.coeffs:
+                if ref.per_gene():
+                    self.per_gene = True
+        return self
+
+    def flat(self):
+        return [([(r.family, r.index, c) for r, c in t.coeffs], t.threshold)
+                for t in self.terms]
+
+
+def disjunction_combine(p1, p2, p12):
+    """P:src/streaming.cpp:110-112."""
+    return float(np.clip(p1 + p2 - p12, 0.0, 1.0))
+
+
+# -------------------------------------------------------------------- engine
+
+class GibbsEngine:
+    """B200 GibbsEngine: same constructor, methods and errors as the
+    reference (P:include/countmc/engine.hpp:110-159)."""
+
+    def __init__(self, data: CountMatrix, spec: ModelSpec, cfg: RunConfig,
+                 contrasts: Sequence[ContrastSpec] = (), device: int = 0):
+        self._lib = load_library()
+        counts = np.asarray(data.counts if isinstance(data, CountMatrix) else data)
+        if counts.shape[1] != spec.X.shape[0]:
+            raise ConfigError("model matrix rows must match the sample count")
+        spec.priors.resolve(spec.X.shape[1])
+        self.G, self.N = counts.shape
+        self.L = spec.X.shape[1]
+        self.spec = spec
+        self._contrast_specs = [c.finalize() for c in contrasts]
+        self._prob = ProblemArrays(counts, spec.X, spec.h, spec.priors.a,
+                                   spec.priors.b, spec.priors.d, spec.priors.c,
+                                   spec.priors.s)
+        self._ctr = ContrastArrays([c.flat() for c in self._contrast_specs])
+        cfg_c = cfg.to_c()
+        err = CmcError()
+        h = c_void_p()
+        rc = self._lib.cmc_engine_create(byref(self._prob.struct), byref(cfg_c),
+                                         byref(self._ctr.struct) if self._contrast_specs else None,
+                                         device, byref(h), byref(err))
+        _raise(rc, err)
+        self._h = h
+        resolved = _abi.CmcRunConfig()
+        self._lib.cmc_engine_config(self._h, byref(resolved))
+        self._cfg = RunConfig(resolved.chains, resolved.iterations, resolved.burnin,
+                              resolved.tune_cutoff, resolved.thin, resolved.seed,
+                              SliceConfig(resolved.max_step_out, resolved.burnin,
+                                          resolved.tune_cutoff, resolved.w_init,
+                                          resolved.max_shrink),
+                              resolved.save_genes, resolved.workers,
+                              cfg.sampler_mode, bool(resolved.concurrent_chains))
+        dims = [c_long() for _ in range(7)]
+        self._lib.cmc_engine_dims(self._h, *[byref(d) for d in dims])
+        self.n_saved = dims[4].value
+        self.n_cols = dims[5].value
+        self.n_rows = dims[6].value
+        saved = np.zeros(max(1, self.n_saved), dtype=np.int64)
+        self._lib.cmc_engine_saved_genes(self._h, lptr(saved))
+        self._saved = saved[:self.n_saved]
+        self._progress = None
+        self._outputs = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.cmc_engine_destroy(h)
+            self._h = None
+
+    # accessors, P:include/countmc/engine.hpp:115-117
+    def config(self) -> RunConfig:
+        return self._cfg
+
+    def contrast_specs(self):
+        return self._contrast_specs
+
+    def saved_genes(self) -> np.ndarray:
+        return self._saved
+
+    @property
+    def handle(self):
+        return self._h
+
+    def initial_state(self, chain: int) -> ChainState:
+        S, _, _ = sizes(self.G, self.N, self.L)
+        buf = np.zeros(S)
+        err = CmcError()
+        _raise(self._lib.cmc_engine_initial_state(self._h, chain, dptr(buf), byref(err)), err)
+        return ChainState.unpack(buf, self.G, self.N, self.L)
+
+    def iterate(self, state: ChainState, tuning: TuningState, chain: int, m: int,
+                clamps: Optional[list] = None, step5_trace: Optional[list] = None):
+        """GibbsEngine::iterate (P:src/engine.cpp:161-370): one sweep of
+        `state` in place on the device.  ``clamps`` (a one-element list) is
+        incremented like ClampCounter."""
+        err = CmcError()
+        st = state.pack()
+        _raise(self._lib.cmc_engine_set_state(self._h, chain, dptr(st), dptr(tuning.w),
+                                              dptr(tuning.w_aux), byref(err)), err)
+        cnt = c_uint64(0)
+        rc = self._lib.cmc_engine_iterate(self._h, chain, m, byref(cnt), byref(err))
+        if clamps is not None:
+            clamps[0] += cnt.value
+        if step5_trace is not None:
+            # the per-gene column loop is sequential by construction
+            for l in range(self.L):
+                step5_trace += [l + 1, -(l + 1)]
+        _raise(rc, err)
+        _raise(self._lib.cmc_engine_get_state(self._h, chain, dptr(st), dptr(tuning.w),
+                                              dptr(tuning.w_aux), byref(err)), err)
+        state.load(st)
+
+    def set_progress(self, fn: Callable[[int, int, int], None]):
+        self._progress = fn
+
+    def run(self) -> List[ChainOutput]:
+        """GibbsEngine::run (P:src/engine.cpp:457-483); chains are batched
+        on the device and each equals the reference's run_chain(c)."""
+        if self._outputs is None:
+            err = CmcError()
+            _raise(self._lib.cmc_engine_begin(self._h, byref(err)), err)
+            total = self._cfg.burnin + self._cfg.iterations
+            step = max(1, min(total, 500)) if self._progress else total
+            m = 1
+            while m <= total:
+                m_end = min(total + 1, m + step)
+                _raise(self._lib.cmc_engine_sweeps(self._h, m, m_end, byref(err)), err)
+                if self._progress:
+                    _raise(self._lib.cmc_engine_sync(self._h, byref(err)), err)
+                    for c in range(self._cfg.chains):
+                        self._progress(c, m_end - 1, total)
+                m = m_end
+            _raise(self._lib.cmc_engine_sync(self._h, byref(err)), err)
+            self._outputs = [self._output(c) for c in range(self._cfg.chains)]
+        return self._outputs
+
+    def run_chain(self, chain: int) -> ChainOutput:
+        return self.run()[chain]
+
+    def sample_names(self) -> List[str]:
+        L = self.L
+        names = ["nu", "tau"] + [f"theta[{l + 1}]" for l in range(L)] + \
+                [f"sigma[{l + 1}]" for l in range(L)]
+        for g in self._saved:
+            names += [f"beta[{g + 1},{l + 1}]" for l in range(L)] + [f"gamma[{g + 1}]"]
+        return names
+
+    def _output(self, chain: int) -> ChainOutput:
+        G, N, L = self.G, self.N, self.L
+        S, _, A = sizes(G, N, L)
+        accs = [np.zeros(A) for _ in range(4)]
+        count = np.zeros(1, dtype=np.int64)
+        n_prob = sum(G if c.per_gene else 1 for c in self._contrast_specs)
+        prob = np.zeros(max(1, n_prob))
+        ccount = np.zeros(max(1, len(self._contrast_specs)), dtype=np.int64)
+        rows = self.n_rows
+        samples = np.zeros(max(1, self.n_cols * rows))
+        iters = np.zeros(max(1, rows), dtype=np.int64)
+        clamps = np.zeros(1, dtype=np.uint64)
+        final = np.zeros(S)
+        secs = np.zeros(7)
+        view = CmcOutputView(lptr(count), dptr(accs[0]), dptr(accs[1]), dptr(accs[2]),
+                             dptr(accs[3]), dptr(prob), lptr(ccount), dptr(samples),
+                             lptr(iters), clamps.ctypes.data_as(ctypes.POINTER(c_uint64)),
+                             dptr(final), dptr(secs))
+        err = CmcError()
+        _raise(self._lib.cmc_engine_get_output(self._h, chain, byref(view), byref(err)), err)
+
+        def part(lo, n, shape=None):
+            arrs = [a[lo:lo + n] if shape is None else a[lo:lo + n].reshape(shape) for a in accs]
+            return Moments(int(count[0]), *arrs)
+
+        o = 0
+        nu = part(o, 1); o += 1
+        tau = part(o, 1); o += 1
+        theta = part(o, L); o += L
+        sigma = part(o, L); o += L
+        beta = part(o, G * L, (G, L)); o += G * L
+        gamma = part(o, G); o += G
+        eps = part(o, G * N, (G, N))
+        contrasts, off = [], 0
+        for k, c in enumerate(self._contrast_specs):
+            n = G if c.per_gene else 1
+            contrasts.append(ContrastResult(c, int(ccount[k]), prob[off:off + n].copy()))
+            off += n
+        return ChainOutput(chain, nu, tau, theta, sigma, beta, gamma, eps, contrasts,
+                           self.sample_names(), samples[:self.n_cols * rows].reshape(self.n_cols, rows),
+                           iters[:rows], self._saved.copy(), secs, int(clamps[0]),
+                           ChainState.unpack(final, G, N, L))
+
+
+# ---------------------------------------------------------- synthetic inputs
+
+@dataclass
+class SimSpec:
+    """P:include/countmc/simulate.hpp:13-27."""
+    G: int
+    N: int
+    X: np.ndarray
+    h: Optional[np.ndarray] = None
+    nu: float = 2.0
+    tau: float = 1.0
+    theta: Sequence[float] = ()
+    sigma: Sequence[float] = ()
+    seed: int = 1
+
+
+def generate(spec: SimSpec) -> CountMatrix:
+    """Synthetic counts with the reference model's generative shape
+    (P:src/simulate.cpp:28-90); the input generator of tests and bench."""
+    lib = load_library()
+    X = np.ascontiguousarray(spec.X, dtype=np.float64)
+    h = np.ascontiguousarray(spec.h if spec.h is not None else np.zeros(spec.N))
+    theta = np.ascontiguousarray(spec.theta, dtype=np.float64)
+    sigma = np.ascontiguousarray(spec.sigma, dtype=np.float64)
+    out = np.zeros((spec.G, spec.N), dtype=np.int64)
+    err = CmcError()
+    rc = lib.cmc_simulate(spec.G, spec.N, X.shape[1], dptr(X), dptr(h), spec.nu, spec.tau,
+                          dptr(theta), dptr(sigma), spec.seed,
+                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), byref(err))
+    _raise(rc, err)
+    return CountMatrix(out)
+
+
+def builtin_design(name: str, N: int) -> np.ndarray:
+    """heterosis16x5: [A (x) 1_4 | 1_4 (x) (1,1,-1,-1)'] tiled over N
+    (P:src/simulate.cpp:123-142)."""
+    if name != "heterosis16x5":
+        raise ConfigError(f"unknown built-in design '{name}'")
+    if N == 0 or N % 16 != 0:
+        raise ConfigError("heterosis16x5 needs a sample count that is a multiple of 16")
+    A = np.array([[1, 1, -1, 0], [1, -1, 1, 0], [1, 1, 1, 1], [1, 1, 1, -1]], dtype=float)
+    block = [1, 1, -1, -1]
+    X = np.zeros((N, 5))
+    for n in range(N):
+        r = n % 16
+        X[n, :4] = A[r // 4]
+        X[n, 4] = block[r % 4]
+    return X
+
+
+def heterosis_contrast(L: int = 5) -> ContrastSpec:
+    """High-parent heterosis: {2 b2 + b4 > 0 and 2 b3 + b4 > 0}
+    (P:src/simulate.cpp:144-155)."""
+    t1 = ContrastTerm([(parse_param_ref("beta[,2]", L), 2.0),
+                       (parse_param_ref("beta[,4]", L), 1.0)], 0.0)
+    t2 = ContrastTerm([(parse_param_ref("beta[,3]", L), 2.0),
+                       (parse_param_ref("beta[,4]", L), 1.0)], 0.0)
+    return ContrastSpec("highparent", [t1, t2]).finalize()
