@@ -200,6 +200,13 @@ void* cmc_engine_stream(cmc_engine* engine);
 /* Kernel launches per sweep (gene kernel + hyper tail [+ contrast]). */
 int cmc_engine_launches_per_sweep(const cmc_engine* engine);
 
+/* Per-kernel timing of `reps` further monitored sweeps (continuing the
+ * run, launched one kernel at a time with CUDA events between them on the
+ * engine stream): average device ms of the fused gene-sweep kernel and of
+ * the reduction/hyper tail per sweep. */
+int cmc_engine_profile(cmc_engine* engine, long m_begin, long reps,
+                       double* gene_ms, double* tail_ms, cmc_error* err);
+
 /* ChainOutput of one chain after run()/sweeps(); see cmc_output_view. */
 int cmc_engine_get_output(cmc_engine* engine, long chain,
                           const cmc_output_view* out, cmc_error* err);

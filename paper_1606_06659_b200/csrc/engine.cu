@@ -311,6 +311,11 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.seed = e->cfg.seed;
   p.K = e->cfg.max_step_out;
   p.max_shrink = e->cfg.max_shrink;
+  {
+    const uint64_t n = (uint64_t)e->cfg.max_step_out + 1;
+    p.k_reject = (0ull - n) % n;
+    p.k_inv = (uint64_t)(((unsigned __int128)1 << 64) / n);
+  }
   p.burnin = e->cfg.burnin;
   p.tune_cutoff = e->cfg.tune_cutoff;
   p.thin = e->cfg.thin;
@@ -1024,6 +1029,55 @@ int cmc_engine_launches_per_sweep(const cmc_engine* e) {
   int n = e->world == 1 ? 3 : 5;
   if (e->has_ctab && e->ctab.gene_needs_hyper) ++n;
   return n;
+}
+
+int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
+                       double* tail_ms, cmc_error* err) {
+  if (!e || reps < 1 || !e->begun) {
+    set_err(err, CMC_ERR_ARG, "profile needs begin() and reps >= 1");
+    return CMC_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(e->device));
+  int rc = set_device_m(e, m_begin, err);
+  if (rc) return rc;
+  SweepParams p = e->base;
+  p.slot_base = 0;
+  p.chain_base = 0;
+  p.monitor_enabled = 1;
+  std::vector<cudaEvent_t> ev((size_t)(3 * reps));
+  for (auto& x : ev) CUDA_TRY(cudaEventCreate(&x));
+  for (long r = 0; r < reps; ++r) {
+    CUDA_TRY(cudaEventRecord(ev[3 * r], e->stream));
+    CUDA_TRY(launch_gene_sweep(p, e->C, r, e->stream));
+    CUDA_TRY(cudaEventRecord(ev[3 * r + 1], e->stream));
+    SweepParams q = p;
+    // the tail: everything enqueue_sweep launches after the gene kernel
+    if (e->world == 1) {
+      CUDA_TRY(launch_leaf_a(q, e->C, r, e->stream));
+      CUDA_TRY(launch_leaf_b(q, e->C, r, e->stream));
+    } else {
+      set_err(err, CMC_ERR_ARG, "profile is single-GPU only");
+      return CMC_ERR_ARG;
+    }
+    if (e->has_ctab && e->ctab.gene_needs_hyper)
+      CUDA_TRY(launch_gene_contrast(q, e->C, r, e->stream));
+    CUDA_TRY(cudaEventRecord(ev[3 * r + 2], e->stream));
+  }
+  CUDA_TRY(launch_advance(e->d_m.p, reps, e->stream));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->host_m = m_begin + reps;
+  double g = 0, t = 0;
+  for (long r = 0; r < reps; ++r) {
+    float a = 0, b = 0;
+    CUDA_TRY(cudaEventElapsedTime(&a, ev[3 * r], ev[3 * r + 1]));
+    CUDA_TRY(cudaEventElapsedTime(&b, ev[3 * r + 1], ev[3 * r + 2]));
+    g += a;
+    t += b;
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  if (gene_ms) *gene_ms = g / reps;
+  if (tail_ms) *tail_ms = t / reps;
+  return check_stall(e, 0, e->C, err);
 }
 
 int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,

@@ -78,14 +78,42 @@ CMC_HD void philox4x64_10(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3,
   out[3] = c3;
 }
 
-// One substream.  The four outputs of the current block are held in
-// registers as a shift queue (no dynamically indexed array, so nothing
-// spills to local memory).
+// Two Philox blocks with interleaved rounds (independent chains: ILP 2).
+CMC_HD void philox4x64_10_x2(uint64_t c0, uint64_t c1, uint64_t blk, uint64_t k0,
+                             uint64_t k1, uint64_t a[4], uint64_t b[4]) {
+  uint64_t x0 = c0, x1 = c1, x2 = blk, x3 = 0;
+  uint64_t y0 = c0, y1 = c1, y2 = blk + 1, y3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    uint64_t hx0, lx0, hx1, lx1, hy0, ly0, hy1, ly1;
+    mulhilo64(0xD2E7470EE14C6C93ull, x0, hx0, lx0);
+    mulhilo64(0xD2E7470EE14C6C93ull, y0, hy0, ly0);
+    mulhilo64(0xCA5A826395121157ull, x2, hx1, lx1);
+    mulhilo64(0xCA5A826395121157ull, y2, hy1, ly1);
+    const uint64_t nx0 = hx1 ^ x1 ^ k0, nx2 = hx0 ^ x3 ^ k1;
+    const uint64_t ny0 = hy1 ^ y1 ^ k0, ny2 = hy0 ^ y3 ^ k1;
+    x0 = nx0; x1 = lx1; x2 = nx2; x3 = lx0;
+    y0 = ny0; y1 = ly1; y2 = ny2; y3 = ly0;
+  }
+  a[0] = x0; a[1] = x1; a[2] = x2; a[3] = x3;
+  b[0] = y0; b[1] = y1; b[2] = y2; b[3] = y3;
+}
+
+// One substream.  Outputs are consumed in order through a register queue
+// (a0..a3, then the pre-generated next block b0..b3); nothing is indexed
+// dynamically, so nothing lives in local memory.  init_x2() generates
+// blocks 0 and 1 up front: a slice step always needs block 0 and usually
+// block 1, and generating both while the warp is converged keeps the
+// 64-bit multiply chains out of the divergent shrink loop.
 struct Stream {
   uint64_t k0, k1, it, site;
-  uint64_t b0, b1, b2, b3;
-  uint32_t block;  // next block index (counter word 2)
-  uint32_t left;   // outputs left in the queue
+  uint64_t a0, a1, a2, a3, b0, b1, b2, b3;
+  uint32_t block;  // next block index (counter word 2) to generate
+  uint32_t na, nb; // outputs left in queue a / block b valid (4 or 0)
 
   CMC_HD void init(uint64_t seed, uint64_t chain, uint64_t iteration,
                    uint64_t site_) {
@@ -94,25 +122,39 @@ struct Stream {
     it = iteration;
     site = site_;
     block = 0;
-    left = 0;
+    na = 0;
+    nb = 0;
+  }
+  CMC_HD void init_x2(uint64_t seed, uint64_t chain, uint64_t iteration,
+                      uint64_t site_) {
+    init(seed, chain, iteration, site_);
+    uint64_t a[4], b[4];
+    philox4x64_10_x2(it, site, 0, k0, k1, a, b);
+    a0 = a[0]; a1 = a[1]; a2 = a[2]; a3 = a[3];
+    b0 = b[0]; b1 = b[1]; b2 = b[2]; b3 = b[3];
+    block = 2;
+    na = 4;
+    nb = 4;
   }
   CMC_HD void refill() {
-    uint64_t o[4];
-    philox4x64_10(it, site, block, 0, k0, k1, o);
-    b0 = o[0];
-    b1 = o[1];
-    b2 = o[2];
-    b3 = o[3];
-    ++block;
-    left = 4;
+    if (nb) {
+      a0 = b0; a1 = b1; a2 = b2; a3 = b3;
+      nb = 0;
+    } else {
+      uint64_t o[4];
+      philox4x64_10(it, site, block, 0, k0, k1, o);
+      a0 = o[0]; a1 = o[1]; a2 = o[2]; a3 = o[3];
+      ++block;
+    }
+    na = 4;
   }
   CMC_HD uint64_t next() {
-    if (left == 0) refill();
-    const uint64_t x = b0;
-    b0 = b1;
-    b1 = b2;
-    b2 = b3;
-    --left;
+    if (na == 0) refill();
+    const uint64_t x = a0;
+    a0 = a1;
+    a1 = a2;
+    a2 = a3;
+    --na;
     return x;
   }
   // ((x >> 11) + 0.5) * 2^-53, P:include/countmc/rng.hpp:38-40.
@@ -125,6 +167,21 @@ struct Stream {
     for (;;) {
       const uint64_t x = next();
       if (x >= reject_below) return x % n;
+    }
+  }
+  // The same draw with 2^64 mod n and floor(2^64 / n) precomputed (n >= 2):
+  // q = mulhi(x, inv) is floor(x/n) or one less, fixed by one compare.
+  CMC_HD uint64_t uniform_int_pre(uint64_t n, uint64_t reject_below,
+                                  uint64_t inv) {
+    for (;;) {
+      const uint64_t x = next();
+      if (x >= reject_below) {
+        uint64_t hi, lo;
+        mulhilo64(x, inv, hi, lo);
+        uint64_t r = x - hi * n;
+        if (r >= n) r -= n;
+        return r;
+      }
     }
   }
 };

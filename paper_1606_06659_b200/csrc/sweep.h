@@ -94,6 +94,7 @@ struct SweepParams {
   int chain_base;  // chain id of grid.y == 0
   int slot_base;   // state slot of grid.y == 0
   int K, max_shrink;
+  uint64_t k_reject, k_inv;  // uniform_int(K+1) constants
   long burnin, tune_cutoff, thin, n_rows, n_cols, n_saved;
   int direct;
   const long* d_m;  // device iteration base; kernels use *d_m + m_off

@@ -38,6 +38,8 @@ struct SliceCfg {
   int max_shrink;
   long burnin;
   long tune_cutoff;
+  uint64_t reject_below;  // 2^64 mod (K+1)
+  uint64_t inv;           // floor(2^64 / (K+1))
 };
 
 // P:include/countmc/slice.hpp:27-35
@@ -66,7 +68,7 @@ __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
   const double wv = w;
   double lo = x0 - wv * rng.u01();
   double hi = lo + wv;
-  uint64_t kl = rng.uniform_int((uint64_t)sc.K + 1);
+  uint64_t kl = rng.uniform_int_pre((uint64_t)sc.K + 1, sc.reject_below, sc.inv);
   uint64_t kr = (uint64_t)sc.K - kl;
   int phase = kl > 0 ? 0 : (kr > 0 ? 1 : 2);
   int it = 0;
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(kGeneBlock)
   const size_t G = (size_t)p.G;
   const uint64_t chain = (uint64_t)(p.chain_base + blockIdx.y);
   const uint64_t gg = (uint64_t)(p.g0 + gl);
-  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff};
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   const size_t so = (size_t)slot;
 
   double* eps = p.eps + so * N * G;
@@ -322,19 +324,24 @@ __global__ void __launch_bounds__(kGeneBlock)
   const double two_gam = 2.0 * gam_old;
   double ss = 0.0;
   for (int n = 0; n < N; ++n) {
-    __syncwarp();
-    if (!alive) continue;
     const size_t i = (size_t)n * G + gl;
     const double hn = __ldg(p.h + n);
-    EpsF f{__ldg(p.y + i), hn + xs[n * kGeneBlock + tid], two_gam, 0u};
-    const double x0 = eps[i];
-    const double w0 = eps_w[i];
-    double w = w0, wa = tuning ? eps_wa[i] : 0.0;
-    Stream rng;
-    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
+    double x0 = 0.0, w0 = 0.0, w = 0.0, wa = 0.0, x1 = 0.0;
     bool st = false;
-    const double x1 = slice_step(f, x0, w, wa, sc, m, rng, st);
-    clamps += f.clamps;
+    __syncwarp();
+    if (alive) {
+      EpsF f{__ldg(p.y + i), hn + xs[n * kGeneBlock + tid], two_gam, 0u};
+      x0 = eps[i];
+      w0 = eps_w[i];
+      w = w0;
+      wa = tuning ? eps_wa[i] : 0.0;
+      Stream rng;
+      rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
+      x1 = slice_step(f, x0, w, wa, sc, m, rng, st);
+      clamps += f.clamps;
+    }
+    __syncwarp();
+    if (!alive) continue;
     if (st) {
       p.stall_x0[so * G + gl] = x0;
       p.stall_w[so * G + gl] = w0;
@@ -353,33 +360,39 @@ __global__ void __launch_bounds__(kGeneBlock)
   }
 
   // Step 2: gamma_g, P:src/engine.cpp:204-226 (nu, tau of iteration m-1)
-  __syncwarp();
-  if (alive) {
-    const double nu = hp->nu, tau = hp->tau;
-    const double shape = (nu + (double)N) / 2.0;
-    const double scale = (nu * tau + ss) / 2.0;
-    Stream rng;
-    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteGamma, gg));
-    double gnew = gam_old;
-    if (p.direct) {
-      gnew = 1.0 / gamma_draw(rng, shape, scale);
-    } else {
-      InvGammaF f{-(shape + 1.0), scale};
-      const double w0 = p.gam_w[so * G + gl];
-      double w = w0, wa = tuning ? p.gam_wa[so * G + gl] : 0.0;
-      bool st = false;
-      gnew = slice_step(f, gam_old, w, wa, sc, m, rng, st);
-      if (st) {
-        p.stall_x0[so * G + gl] = gam_old;
-        p.stall_w[so * G + gl] = w0;
-        record_stall(hp, stall_key(2, 0, gg, 0), m);
-        alive = false;
-      } else if (tuning) {
+  {
+    double gnew = gam_old, w0 = 0.0, w = 0.0, wa = 0.0;
+    bool st = false;
+    __syncwarp();
+    if (alive) {
+      const double nu = hp->nu, tau = hp->tau;
+      const double shape = (nu + (double)N) / 2.0;
+      const double scale = (nu * tau + ss) / 2.0;
+      Stream rng;
+      if (p.direct) {
+        rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteGamma, gg));
+        gnew = 1.0 / gamma_draw(rng, shape, scale);
+      } else {
+        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteGamma, gg));
+        InvGammaF f{-(shape + 1.0), scale};
+        w0 = p.gam_w[so * G + gl];
+        w = w0;
+        wa = tuning ? p.gam_wa[so * G + gl] : 0.0;
+        gnew = slice_step(f, gam_old, w, wa, sc, m, rng, st);
+      }
+    }
+    __syncwarp();
+    if (alive && st) {
+      p.stall_x0[so * G + gl] = gam_old;
+      p.stall_w[so * G + gl] = w0;
+      record_stall(hp, stall_key(2, 0, gg, 0), m);
+      alive = false;
+    }
+    if (alive) {
+      if (tuning && !p.direct) {
         p.gam_w[so * G + gl] = w;
         p.gam_wa[so * G + gl] = wa;
       }
-    }
-    if (alive) {
       p.gam[so * G + gl] = gnew;
       p.log_gam[so * G + gl] = log(gnew);
       p.inv_gam[so * G + gl] = 1.0 / gnew;
@@ -389,37 +402,42 @@ __global__ void __launch_bounds__(kGeneBlock)
 
   // Step 5: beta_g1..beta_gL in column order, P:src/engine.cpp:269-334
   for (int l = 0; l < L; ++l) {
+    const size_t i = (size_t)l * G + gl;
+    const int jb = __ldg(p.grp_off + l), je = __ldg(p.grp_off + l + 1);
+    double bold = 0.0, bnew = 0.0, w0 = 0.0, w = 0.0, wa = 0.0;
+    bool st = false;
+    __syncwarp();
+    if (alive) {
+      bold = beta[i];
+      for (int j = jb; j < je; ++j) {
+        const double v = __ldg(p.grp_val + j);
+        double s = 0.0;
+        for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
+          const int n = __ldg(p.grp_mem + q);
+          double t = xs[n * kGeneBlock + tid] - v * bold;
+          if (t > kExpClamp) {
+            ++clamps;
+            t = kExpClamp;
+          }
+          s += exp(t);
+        }
+        sS[(j - jb) * kGeneBlock + tid] = s;
+        sLogS[(j - jb) * kGeneBlock + tid] = log(s);
+      }
+      const double sig = hp->sigma[l];
+      const double sig2 = sig * sig;
+      BetaF f{__ldg(p.A + i), hp->theta[l], 2.0 * sig2, p.exp_clamp,
+              p.grp_val + jb, sS + tid, sLogS + tid, je - jb, 0u};
+      w0 = beta_w[i];
+      w = w0;
+      wa = tuning ? beta_wa[i] : 0.0;
+      Stream rng;
+      rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l));
+      bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
+      clamps += f.clamps;
+    }
     __syncwarp();
     if (!alive) continue;
-    const size_t i = (size_t)l * G + gl;
-    const double bold = beta[i];
-    const int jb = __ldg(p.grp_off + l), je = __ldg(p.grp_off + l + 1);
-    for (int j = jb; j < je; ++j) {
-      const double v = __ldg(p.grp_val + j);
-      double s = 0.0;
-      for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
-        const int n = __ldg(p.grp_mem + q);
-        double t = xs[n * kGeneBlock + tid] - v * bold;
-        if (t > kExpClamp) {
-          ++clamps;
-          t = kExpClamp;
-        }
-        s += exp(t);
-      }
-      sS[(j - jb) * kGeneBlock + tid] = s;
-      sLogS[(j - jb) * kGeneBlock + tid] = log(s);
-    }
-    const double sig = hp->sigma[l];
-    const double sig2 = sig * sig;
-    BetaF f{__ldg(p.A + i), hp->theta[l], 2.0 * sig2, p.exp_clamp,
-            p.grp_val + jb, sS + tid, sLogS + tid, je - jb, 0u};
-    const double w0 = beta_w[i];
-    double w = w0, wa = tuning ? beta_wa[i] : 0.0;
-    Stream rng;
-    rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l));
-    bool st = false;
-    const double bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
-    clamps += f.clamps;
     if (st) {
       p.stall_x0[so * G + gl] = bold;
       p.stall_w[so * G + gl] = w0;
@@ -487,14 +505,14 @@ __device__ __forceinline__ double warp_leaf_sum(V value, long start, long end) {
     const long idx = start + c * 32 + lane;
     v[c] = idx < end ? value(idx) : 0.0;
   }
+  // Padding past the leaf end with +0.0 is exact: the running sum starts at
+  // +0.0 and can never become -0.0, so s + 0.0 == s.
+  (void)n;
   double s = 0.0;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double vj = __shfl_sync(0xffffffffu, v[c], j);
-      if (c * 32 + j < n) s += vj;
-    }
+    for (int j = 0; j < 32; ++j) s += __shfl_sync(0xffffffffu, v[c], j);
   }
   return s;
 }
@@ -559,7 +577,7 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const uint64_t chain = (uint64_t)(p.chain_base + (slot - p.slot_base));
   const int L = p.L, Q = 2 + L;
-  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff};
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   const double Gd = (double)p.G_total;
   if (warp < Q) {
     const double r = warp_pairwise_leaves(p.partA, p, slot, Q, warp, p.n_leaves_total);
@@ -634,7 +652,7 @@ __device__ void hyper_b_body(const SweepParams& p, int slot, long m) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const uint64_t chain = (uint64_t)(p.chain_base + (slot - p.slot_base));
   const int L = p.L;
-  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff};
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   if (warp < L) {
     const double r = warp_pairwise_leaves(p.partB, p, slot, L, warp, p.n_leaves_total);
     if ((tid & 31) == 0) red[warp] = r;

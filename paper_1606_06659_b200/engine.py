@@ -385,6 +385,24 @@ class GibbsEngine:
             self._lib.cmc_engine_destroy(h)
             self._h = None
 
+    def shard(self, rank: int, world: int, nccl_uid: bytes = b""):
+        """Restrict this engine to its leaf-aligned gene shard and join the
+        NCCL clique (one process per GPU).  Must precede any sweep."""
+        err = CmcError()
+        buf = ctypes.create_string_buffer(bytes(nccl_uid).ljust(128, b"\0"), 128)
+        _raise(self._lib.cmc_engine_shard(self._h, rank, world, buf, byref(err)), err)
+        lo, hi = c_long(), c_long()
+        self._lib.cmc_shard_bounds(self.G, rank, world, byref(lo), byref(hi))
+        self.shard_range = (lo.value, hi.value)
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = load_library()
+        buf = ctypes.create_string_buffer(128)
+        err = CmcError()
+        _raise(lib.cmc_nccl_unique_id(buf, byref(err)), err)
+        return buf.raw
+
     # accessors, P:include/countmc/engine.hpp:115-117
     def config(self) -> RunConfig:
         return self._cfg
