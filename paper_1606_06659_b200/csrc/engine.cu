@@ -865,7 +865,7 @@ int cmc_engine_initial_state(const cmc_engine* e, long chain, double* state,
 
 int cmc_engine_set_state(cmc_engine* e, long chain, const double* state,
                          const double* tw, const double* ta, cmc_error* err) {
-  if (!e || !state || chain < 0 || chain >= e->C) {
+  if (!e || !state || chain < 0) {
     set_err(err, CMC_ERR_ARG, "bad chain or state");
     return CMC_ERR_ARG;
   }
@@ -873,12 +873,14 @@ int cmc_engine_set_state(cmc_engine* e, long chain, const double* state,
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
-  return upload_state(e, chain, state, tw, ta, err);
+  // the reference's iterate() takes any chain id: state lives in slot
+  // chain mod C, the chain id only keys the random stream
+  return upload_state(e, chain % e->C, state, tw, ta, err);
 }
 
 int cmc_engine_get_state(cmc_engine* e, long chain, double* state, double* tw,
                          double* ta, cmc_error* err) {
-  if (!e || chain < 0 || chain >= e->C) {
+  if (!e || chain < 0) {
     set_err(err, CMC_ERR_ARG, "bad chain");
     return CMC_ERR_ARG;
   }
@@ -886,12 +888,12 @@ int cmc_engine_get_state(cmc_engine* e, long chain, double* state, double* tw,
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
-  return download_state(e, chain, state, tw, ta, err);
+  return download_state(e, chain % e->C, state, tw, ta, err);
 }
 
 int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
                        cmc_error* err) {
-  if (!e || chain < 0 || chain >= e->C || m < 1) {
+  if (!e || chain < 0 || m < 1) {
     set_err(err, CMC_ERR_ARG, "bad chain or iteration");
     return CMC_ERR_ARG;
   }
@@ -899,21 +901,22 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(e->device));
   if ((rc = set_device_m(e, m, err))) return rc;
+  const long slot = chain % e->C;
   Hyper hp;
-  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + chain, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + slot, sizeof(Hyper), cudaMemcpyDeviceToHost));
   const unsigned long long before = hp.clamps;
   hp.err_key = kNoError;
-  CUDA_TRY(cudaMemcpy(&e->hyper.p[chain].err_key, &hp.err_key,
+  CUDA_TRY(cudaMemcpy(&e->hyper.p[slot].err_key, &hp.err_key,
                       sizeof(unsigned long long), cudaMemcpyHostToDevice));
   SweepParams p = e->base;
-  p.slot_base = (int)chain;
+  p.slot_base = (int)slot;
   p.chain_base = (int)chain;
   p.monitor_enabled = 0;
   CUDA_TRY(enqueue_sweep(e, p, 1, 0));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
-  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + chain, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + slot, sizeof(Hyper), cudaMemcpyDeviceToHost));
   if (clamps) *clamps += hp.clamps - before;
-  if (hp.err_key != kNoError) return check_stall(e, chain, chain + 1, err);
+  if (hp.err_key != kNoError) return check_stall(e, slot, slot + 1, err);
   return CMC_OK;
 }
 

@@ -72,6 +72,21 @@ class Product:
         if getattr(self, "h", None):
             self.lib.cmc_engine_destroy(self.h)
 
+    def initial_state(self, chain):
+        S, _, _ = sizes(self.G, self.N, self.L)
+        st = np.zeros(S)
+        err = CmcError()
+        assert self.lib.cmc_engine_initial_state(self.h, chain, dptr(st), byref(err)) == 0
+        return st
+
+    def saved_genes(self):
+        from ctypes import c_long
+        dims = [c_long() for _ in range(7)]
+        self.lib.cmc_engine_dims(self.h, *[byref(d) for d in dims])
+        out = np.zeros(max(1, dims[4].value), np.int64)
+        self.lib.cmc_engine_saved_genes(self.h, out.ctypes.data_as(__import__("ctypes").POINTER(c_long)))
+        return out[:dims[4].value]
+
     def iterate(self, st, tw, ta, chain, m):
         err = CmcError()
         rc = self.lib.cmc_engine_set_state(self.h, chain, dptr(st), dptr(tw), dptr(ta), byref(err))
