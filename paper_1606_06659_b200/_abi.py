@@ -14,7 +14,7 @@ from ctypes import (POINTER, c_char, c_double, c_int, c_long, c_longlong,
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libcountmc_b200.so")
+LIB_PATH = os.environ.get("CMC_LIB_OVERRIDE") or os.path.join(HERE, "lib", "libcountmc_b200.so")
 
 CMC_OK = 0
 CMC_ERR_CONFIG = 1

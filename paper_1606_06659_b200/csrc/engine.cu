@@ -172,7 +172,7 @@ struct cmc_engine {
   DevBuf<int> goff, gmoff, gmem, saved_slot;
   DevBuf<double> eps, eps_w, eps_wa, gam, gam_w, gam_wa, beta, beta_w, beta_wa;
   DevBuf<double> log_gam, inv_gam, acc_eps, acc_gam, acc_beta, cprob, samples;
-  DevBuf<double> partA, partB, stall_x0, stall_w;
+  DevBuf<double> partA, partB;
   DevBuf<Hyper> hyper;
   DevBuf<ContrastTable> dctab;
   DevBuf<long> d_m;
@@ -263,8 +263,6 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(e->acc_beta.alloc(4 * gl));
   CUDA_TRY(e->cprob.alloc(std::max<long>(1, prob_len(e)) * C));
   CUDA_TRY(e->samples.alloc(std::max<long>(1, e->n_cols * e->n_rows) * C));
-  CUDA_TRY(e->stall_x0.alloc(gc));
-  CUDA_TRY(e->stall_w.alloc(gc));
   CUDA_TRY(e->hyper.alloc((size_t)C));
   CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * C));
   const long n_leaves_total = (e->G_total + kLeaf - 1) / kLeaf;
@@ -348,8 +346,6 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.partA = e->partA.p;
   p.partB = e->partB.p;
   p.C = (int)C;
-  p.stall_x0 = e->stall_x0.p;
-  p.stall_w = e->stall_w.p;
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->dev_ready = true;
   return CMC_OK;
@@ -532,11 +528,16 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
     const long n = (long)(hp.err_key & 0xfffff);
     double x0 = 0, w = 0;
     if (step == 1 || step == 2 || step == 5) {
-      const long gl = g - e->g0;
-      CUDA_TRY(cudaMemcpy(&x0, e->stall_x0.p + c * e->G + gl, sizeof(double),
-                          cudaMemcpyDeviceToHost));
-      CUDA_TRY(cudaMemcpy(&w, e->stall_w.p + c * e->G + gl, sizeof(double),
-                          cudaMemcpyDeviceToHost));
+      // a stalled step leaves its value and width untouched on the device
+      const size_t gl = (size_t)(g - e->g0), G = (size_t)e->G;
+      const double* xs = step == 1 ? e->eps.p + (size_t)c * e->N * G + (size_t)n * G + gl
+                         : step == 2 ? e->gam.p + (size_t)c * G + gl
+                                     : e->beta.p + (size_t)c * e->L * G + (size_t)col * G + gl;
+      const double* ws = step == 1 ? e->eps_w.p + (size_t)c * e->N * G + (size_t)n * G + gl
+                         : step == 2 ? e->gam_w.p + (size_t)c * G + gl
+                                     : e->beta_w.p + (size_t)c * e->L * G + (size_t)col * G + gl;
+      CUDA_TRY(cudaMemcpy(&x0, xs, sizeof(double), cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(&w, ws, sizeof(double), cudaMemcpyDeviceToHost));
     } else {
       const int k = step == 3 ? 0 : step == 4 ? 1 : 2 + (int)col;
       x0 = hp.err_x0[k];
@@ -559,8 +560,9 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
 // Enqueue one sweep (iteration *d_m + off) for grid.y chains at slot_base.
 cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
                           long off) {
-  cudaError_t r = launch_gene_sweep(p, chains, off, e->stream);
+  cudaError_t r = launch_eps_sweep(p, chains, off, e->stream);
   if (r != cudaSuccess) return r;
+  if ((r = launch_gene_sweep(p, chains, off, e->stream)) != cudaSuccess) return r;
   if (e->world == 1) {
     if ((r = launch_leaf_a(p, chains, off, e->stream)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, e->stream)) != cudaSuccess) return r;
@@ -810,7 +812,7 @@ int cmc_engine_destroy(cmc_engine* e) {
                             &e->gam_wa, &e->beta, &e->beta_w, &e->beta_wa,
                             &e->log_gam, &e->inv_gam, &e->acc_eps, &e->acc_gam,
                             &e->acc_beta, &e->cprob, &e->samples, &e->partA,
-                            &e->partB, &e->stall_x0, &e->stall_w};
+                            &e->partB};
     for (auto* b : ds) b->free_();
     e->goff.free_();
     e->gmoff.free_();
@@ -1029,7 +1031,7 @@ void* cmc_engine_stream(cmc_engine* e) {
 
 int cmc_engine_launches_per_sweep(const cmc_engine* e) {
   if (!e) return 0;
-  int n = e->world == 1 ? 3 : 5;
+  int n = e->world == 1 ? 4 : 6;
   if (e->has_ctab && e->ctab.gene_needs_hyper) ++n;
   return n;
 }
@@ -1051,6 +1053,7 @@ int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
   for (auto& x : ev) CUDA_TRY(cudaEventCreate(&x));
   for (long r = 0; r < reps; ++r) {
     CUDA_TRY(cudaEventRecord(ev[3 * r], e->stream));
+    CUDA_TRY(launch_eps_sweep(p, e->C, r, e->stream));
     CUDA_TRY(launch_gene_sweep(p, e->C, r, e->stream));
     CUDA_TRY(cudaEventRecord(ev[3 * r + 1], e->stream));
     SweepParams q = p;

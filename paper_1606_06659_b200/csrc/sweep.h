@@ -116,10 +116,11 @@ struct SweepParams {
   double* partA;  // [world][C][2+L][leaves_per_rank]
   double* partB;  // [world][C][L][leaves_per_rank]
   int C;          // chains resident (stride of the partial buffers)
-  double *stall_x0, *stall_w;  // [C][G]
 };
 
 // Launch wrappers (sweep_kernels.cu).  `chains` = grid.y.
+cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
+                             cudaStream_t s);
 cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
                               cudaStream_t s);
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,

@@ -24,6 +24,7 @@
 // sampled values bit-identical to the reference for identical uniforms.
 #include <math.h>
 
+#include "fastmath.cuh"
 #include "rng.cuh"
 #include "sweep.h"
 
@@ -57,7 +58,10 @@ __device__ __forceinline__ void tune_update(double& w, double& wa, long m,
 // (P:include/countmc/slice.hpp:42-75), written as ONE loop that performs
 // one log-density evaluation per trip whatever phase (step-out left,
 // step-out right, shrink) a lane is in: a warp pays the maximum of the
-// lanes' total evaluation counts, not the sum of per-phase maxima.
+// lanes' total evaluation counts, not the sum of per-phase maxima.  The
+// trip body is branch-free (each lane computes every phase's update and
+// keeps the one its phase selects), so diverged lanes still issue as one
+// SIMT stream; only the rare refill of a third Philox block branches.
 template <class F>
 __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
                                              double& wa, const SliceCfg& sc,
@@ -68,44 +72,42 @@ __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
   const double wv = w;
   double lo = x0 - wv * rng.u01();
   double hi = lo + wv;
-  uint64_t kl = rng.uniform_int_pre((uint64_t)sc.K + 1, sc.reject_below, sc.inv);
-  uint64_t kr = (uint64_t)sc.K - kl;
+  const int kl0 = (int)rng.uniform_int_pre((uint64_t)sc.K + 1, sc.reject_below, sc.inv);
+  int kl = kl0, kr = sc.K - kl0;
   int phase = kl > 0 ? 0 : (kr > 0 ? 1 : 2);
   int it = 0;
   double x1 = x0;
   for (;;) {
-    double xe;
-    if (phase == 2) {
-      x1 = lo + (hi - lo) * rng.u01();
-      xe = x1;
-    } else {
-      xe = phase == 0 ? lo : hi;
+    const bool S = phase == 2;
+    if (S && rng.na == 0) rng.refill();
+    const double u = ((double)(rng.a0 >> 11) + 0.5) * 0x1.0p-53;
+    if (S) {  // pop (predicated moves)
+      rng.a0 = rng.a1;
+      rng.a1 = rng.a2;
+      rng.a2 = rng.a3;
+      --rng.na;
     }
+    const double xs = lo + (hi - lo) * u;
+    const double xe = S ? xs : (phase == 0 ? lo : hi);
     const double fe = f(xe);
-    if (phase == 0) {
-      if (logu < fe) {
-        lo -= wv;
-        if (--kl == 0) phase = kr > 0 ? 1 : 2;
-      } else {
-        phase = kr > 0 ? 1 : 2;
-      }
-    } else if (phase == 1) {
-      if (logu < fe) {
-        hi += wv;
-        if (--kr == 0) phase = 2;
-      } else {
-        phase = 2;
-      }
-    } else {
-      if (fe > logu) break;
-      if (x1 > x0)
-        hi = x1;
-      else
-        lo = x1;
-      if (++it >= sc.max_shrink) {
-        stalled = true;
-        return x0;
-      }
+    const bool Lp = phase == 0, Rp = phase == 1;
+    const bool in = logu < fe;
+    const bool acc = S && (fe > logu);
+    const bool rej = S && !(fe > logu);
+    lo = (Lp && in) ? lo - wv : lo;
+    hi = (Rp && in) ? hi + wv : hi;
+    kl -= (Lp && in) ? 1 : 0;
+    kr -= (Rp && in) ? 1 : 0;
+    hi = (rej && xs > x0) ? xs : hi;
+    lo = (rej && !(xs > x0)) ? xs : lo;
+    it += rej ? 1 : 0;
+    x1 = S ? xs : x1;
+    const int after_l = kr > 0 ? 1 : 2;
+    phase = (Lp && !(in && kl > 0)) ? after_l : ((Rp && !(in && kr > 0)) ? 2 : phase);
+    if (acc) break;
+    if (it >= sc.max_shrink) {
+      stalled = true;
+      return x0;
     }
   }
   if (m <= sc.burnin) tune_update(w, wa, m, fabs(x1 - x0), sc.tune_cutoff);
@@ -115,7 +117,8 @@ __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
 // log full conditional of eps_gn, P:src/model.cpp:70-74 (clamped_exp
 // :13-19): y*e - exp(min(h + eta + e, 700)) - e*e / (2 gamma).
 struct EpsF {
-  double y, cn, two_gam;
+  double y, cn, inv_two_gam;
+  const double* tab;
   unsigned clamps;
   __device__ __forceinline__ double operator()(double x) {
     double t = cn + x;
@@ -123,7 +126,7 @@ struct EpsF {
       ++clamps;
       t = kExpClamp;
     }
-    return y * x - exp(t) - x * x / two_gam;
+    return y * x - fast_exp(t, tab) - x * x * inv_two_gam;
   }
 };
 
@@ -167,10 +170,11 @@ struct SigmaF {
 // Grouped beta density, P:src/engine.cpp:303-316: exp(base + v b) is
 // factored as S_j exp(v_j b) over the distinct nonzero column values.
 struct BetaF {
-  double a, theta, two_sig2, e700;
+  double a, theta, inv_two_sig2, e700;
   const double* val;   // group values (uniform across the warp)
   const double* S;     // shared memory, stride kGeneBlock
   const double* logS;
+  const double* tab;
   int J;
   unsigned clamps;
   __device__ __forceinline__ double operator()(double b) {
@@ -183,11 +187,11 @@ struct BetaF {
         ++clamps;
         tot -= e700;
       } else if (Sj > 0.0) {
-        tot -= Sj * exp(t);
+        tot -= Sj * fast_exp(t, tab);
       }
     }
     const double zz = b - theta;
-    return tot - zz * zz / two_sig2;
+    return tot - zz * zz * inv_two_sig2;
   }
 };
 
@@ -274,13 +278,79 @@ __device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
 
 // ---------------------------------------------------------------- kernels
 
-// One thread per gene.  Lanes of a warp are re-converged with __syncwarp()
-// at every slice-step boundary so each step's log-density evaluations run
-// as one SIMT stream (no early exits: a lane without a gene, or whose gene
-// stalled, idles with alive == false).
-__global__ void __launch_bounds__(kGeneBlock)
+// Step 1, one thread per (gene, sample): eps_gn are conditionally
+// independent given the gene's previous beta and gamma (P:src/engine.cpp:
+// 178-202), so the 16 slice steps of a gene run on 16 threads.  A warp holds
+// 32 consecutive genes at one sample n (coalesced SoA loads), the grid's y
+// dimension is n and z the chain.  Everything a step needs fits in
+// registers, so occupancy is high and the tail wave is short.
+#ifndef CMC_EPS_MIN_BLOCKS
+#define CMC_EPS_MIN_BLOCKS 6
+#endif
+__global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
+    eps_sweep_kernel(const SweepParams p, const long m_off) {
+  __shared__ double exp_tab[32];
+  exp_table_init(exp_tab);
+  __syncthreads();
+  const int slot = p.slot_base + blockIdx.z;
+  Hyper* hp = p.hyper + slot;
+  if (hp->err_key != kNoError) return;
+  const long gl = (long)blockIdx.x * kGeneBlock + threadIdx.x;
+  if (gl >= p.G) return;
+  const int n = blockIdx.y;
+  const long m = *p.d_m + m_off;
+  const bool tuning = m <= p.burnin;
+  const int N = p.N, L = p.L;
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const uint64_t chain = (uint64_t)(p.chain_base + blockIdx.z);
+  const uint64_t gg = (uint64_t)(p.g0 + gl);
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
+  const size_t i = (size_t)n * G + gl;
+  const size_t ie = so * N * G + i;
+
+  // xb_gn = sum_l X_nl beta_gl, l ascending from 0.0 (refresh_xb,
+  // P:src/engine.cpp:144-159)
+  const double* beta = p.beta + so * L * G;
+  double xb = 0.0;
+  for (int l = 0; l < L; ++l) xb += __ldg(p.X + n * L + l) * beta[(size_t)l * G + gl];
+  const double inv_two_gam = 1.0 / (2.0 * p.gam[so * G + gl]);
+  EpsF f{__ldg(p.y + i), __ldg(p.h + n) + xb, inv_two_gam, exp_tab, 0u};
+  const double x0 = p.eps[ie];
+  double w = p.eps_w[ie];
+  double wa = tuning ? p.eps_wa[ie] : 0.0;
+  Stream rng;
+  rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
+  bool st = false;
+  const double x1 = slice_step(f, x0, w, wa, sc, m, rng, st);
+  if (st) {
+    // eps and its width stay untouched: the host reads x0 and w back
+    record_stall(hp, stall_key(1, 0, gg, n), m);
+  } else {
+    p.eps[ie] = x1;
+    if (tuning) {
+      p.eps_w[ie] = w;
+      p.eps_wa[ie] = wa;
+    }
+    if (p.monitor_enabled && m > p.burnin)
+      moments(p.acc_eps + so * 4 * N * G + i, (size_t)N * G, x1, (double)(m - p.burnin));
+  }
+  if (f.clamps) atomicAdd(&hp->clamps, (unsigned long long)f.clamps);
+}
+
+// Steps 2 and 5, one thread per gene: gamma_g from the new eps row, then
+// beta_g1..beta_gL in column order.  Lanes of a warp are re-converged with
+// __syncwarp() at every slice-step boundary so each step's log-density
+// evaluations run as one SIMT stream (no early exits: a lane without a
+// gene, or whose gene stalled, idles with alive == false).
+#ifndef CMC_GENE_MIN_BLOCKS
+#define CMC_GENE_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
     gene_sweep_kernel(const SweepParams p, const long m_off) {
   extern __shared__ double smem[];
+  __shared__ double exp_tab[32];
+  exp_table_init(exp_tab);
+  __syncthreads();
   const int tid = threadIdx.x;
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
@@ -300,63 +370,30 @@ __global__ void __launch_bounds__(kGeneBlock)
   const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   const size_t so = (size_t)slot;
 
-  double* eps = p.eps + so * N * G;
-  double* eps_w = p.eps_w + so * N * G;
-  double* eps_wa = p.eps_wa + so * N * G;
+  const double* eps = p.eps + so * N * G;
   double* beta = p.beta + so * L * G;
   double* beta_w = p.beta_w + so * L * G;
   double* beta_wa = p.beta_wa + so * L * G;
-  double* xs = smem;                             // [N][B]: xb, then lp
+  double* xs = smem;                             // [N][B]: lp
   double* sS = smem + (size_t)N * kGeneBlock;    // [Jmax][B]
   double* sLogS = sS + (size_t)p.Jmax * kGeneBlock;
   unsigned clamps = 0;
 
-  // refresh_xb, P:src/engine.cpp:144-159 (l ascending from 0.0 per n)
+  // lp_n = (h_n + eps_n) + xb_n with the new eps and the previous beta,
+  // and ss = sum_n eps_n^2 in n order (P:src/engine.cpp:275-283,
+  // P:src/model.cpp:76-82)
   for (int n = 0; n < N; ++n) xs[n * kGeneBlock + tid] = 0.0;
   for (int l = 0; l < L; ++l) {
     const double b = alive ? beta[(size_t)l * G + gl] : 0.0;
     for (int n = 0; n < N; ++n)
       xs[n * kGeneBlock + tid] += __ldg(p.X + n * L + l) * b;
   }
-
-  // Step 1: eps_gn, P:src/engine.cpp:178-202
   const double gam_old = alive ? p.gam[so * G + gl] : 1.0;
-  const double two_gam = 2.0 * gam_old;
   double ss = 0.0;
   for (int n = 0; n < N; ++n) {
-    const size_t i = (size_t)n * G + gl;
-    const double hn = __ldg(p.h + n);
-    double x0 = 0.0, w0 = 0.0, w = 0.0, wa = 0.0, x1 = 0.0;
-    bool st = false;
-    __syncwarp();
-    if (alive) {
-      EpsF f{__ldg(p.y + i), hn + xs[n * kGeneBlock + tid], two_gam, 0u};
-      x0 = eps[i];
-      w0 = eps_w[i];
-      w = w0;
-      wa = tuning ? eps_wa[i] : 0.0;
-      Stream rng;
-      rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
-      x1 = slice_step(f, x0, w, wa, sc, m, rng, st);
-      clamps += f.clamps;
-    }
-    __syncwarp();
-    if (!alive) continue;
-    if (st) {
-      p.stall_x0[so * G + gl] = x0;
-      p.stall_w[so * G + gl] = w0;
-      record_stall(hp, stall_key(1, 0, gg, n), m);
-      alive = false;
-      continue;
-    }
-    eps[i] = x1;
-    if (tuning) {
-      eps_w[i] = w;
-      eps_wa[i] = wa;
-    }
-    ss += x1 * x1;
-    xs[n * kGeneBlock + tid] = hn + x1 + xs[n * kGeneBlock + tid];  // lp
-    if (monitor) moments(p.acc_eps + so * 4 * N * G + i, (size_t)N * G, x1, mcount);
+    const double e = alive ? eps[(size_t)n * G + gl] : 0.0;
+    ss += e * e;
+    xs[n * kGeneBlock + tid] = __ldg(p.h + n) + e + xs[n * kGeneBlock + tid];
   }
 
   // Step 2: gamma_g, P:src/engine.cpp:204-226 (nu, tau of iteration m-1)
@@ -383,8 +420,6 @@ __global__ void __launch_bounds__(kGeneBlock)
     }
     __syncwarp();
     if (alive && st) {
-      p.stall_x0[so * G + gl] = gam_old;
-      p.stall_w[so * G + gl] = w0;
       record_stall(hp, stall_key(2, 0, gg, 0), m);
       alive = false;
     }
@@ -419,15 +454,15 @@ __global__ void __launch_bounds__(kGeneBlock)
             ++clamps;
             t = kExpClamp;
           }
-          s += exp(t);
+          s += fast_exp(t, exp_tab);
         }
         sS[(j - jb) * kGeneBlock + tid] = s;
         sLogS[(j - jb) * kGeneBlock + tid] = log(s);
       }
       const double sig = hp->sigma[l];
       const double sig2 = sig * sig;
-      BetaF f{__ldg(p.A + i), hp->theta[l], 2.0 * sig2, p.exp_clamp,
-              p.grp_val + jb, sS + tid, sLogS + tid, je - jb, 0u};
+      BetaF f{__ldg(p.A + i), hp->theta[l], 1.0 / (2.0 * sig2), p.exp_clamp,
+              p.grp_val + jb, sS + tid, sLogS + tid, exp_tab, je - jb, 0u};
       w0 = beta_w[i];
       w = w0;
       wa = tuning ? beta_wa[i] : 0.0;
@@ -439,8 +474,6 @@ __global__ void __launch_bounds__(kGeneBlock)
     __syncwarp();
     if (!alive) continue;
     if (st) {
-      p.stall_x0[so * G + gl] = bold;
-      p.stall_w[so * G + gl] = w0;
       record_stall(hp, stall_key(5, l, gg, 0), m);
       alive = false;
       continue;
@@ -843,6 +876,13 @@ __global__ void compute_A_kernel(const double* y, const double* X, double* A,
 
 int gene_sweep_smem_bytes(int N, int Jmax) {
   return (int)(sizeof(double) * (size_t)(N + 2 * Jmax) * kGeneBlock);
+}
+
+cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
+                             cudaStream_t s) {
+  dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)p.N, (unsigned)chains);
+  eps_sweep_kernel<<<grid, kGeneBlock, 0, s>>>(p, m_off);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
