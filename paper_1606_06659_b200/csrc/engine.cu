@@ -167,6 +167,9 @@ struct cmc_engine {
   int device = 0;
   bool dev_ready = false;
   cudaStream_t stream = nullptr;
+  cudaStream_t tail_stream = nullptr;  // reduction/hyper tail, overlaps the
+                                       // next iteration's eps kernel
+  cudaEvent_t ev_gene = nullptr, ev_tail = nullptr;
   int C = 1;
   DevBuf<double> y, A, Xd, hd, gval;
   DevBuf<int> goff, gmoff, gmem, saved_slot;
@@ -202,6 +205,9 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   if (e->dev_ready) return CMC_OK;
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&e->tail_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&e->ev_gene, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&e->ev_tail, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreate(&e->ev0));
   CUDA_TRY(cudaEventCreate(&e->ev1));
   const long G = e->G, N = e->N, L = e->L, C = e->C;
@@ -460,6 +466,7 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
     hp.wa_tau = ta[off + L + 1];
   }
   hp.err_key = kNoError;
+  hp.err_key_eps = kNoError;
   hp.doneA = hp.doneB = 0;
   CUDA_TRY(cudaMemcpy(e->hyper.p + c, &hp, sizeof(Hyper), cudaMemcpyHostToDevice));
   return CMC_OK;
@@ -521,11 +528,22 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
   for (long c = slot_lo; c < slot_hi; ++c) {
     Hyper hp;
     CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + c, sizeof(Hyper), cudaMemcpyDeviceToHost));
-    if (hp.err_key == kNoError) continue;
-    const unsigned step = (unsigned)(hp.err_key >> 60);
-    const long col = (long)((hp.err_key >> 52) & 0xff);
-    const long g = (long)((hp.err_key >> 20) & 0xffffffffull);
-    const long n = (long)(hp.err_key & 0xfffff);
+    if (hp.err_key == kNoError && hp.err_key_eps == kNoError) continue;
+    // two slots (see sweep_kernels.cu record_stall): the earlier iteration
+    // wins, then the smaller key (the reference's sequential order)
+    unsigned long long key = hp.err_key;
+    long long km = hp.err_m;
+    if (hp.err_key_eps != kNoError &&
+        (hp.err_key == kNoError || hp.err_m_eps < hp.err_m ||
+         (hp.err_m_eps == hp.err_m && hp.err_key_eps < hp.err_key))) {
+      key = hp.err_key_eps;
+      km = hp.err_m_eps;
+    }
+    hp.err_m = km;
+    const unsigned step = (unsigned)(key >> 60);
+    const long col = (long)((key >> 52) & 0xff);
+    const long g = (long)((key >> 20) & 0xffffffffull);
+    const long n = (long)(key & 0xfffff);
     double x0 = 0, w = 0;
     if (step == 1 || step == 2 || step == 5) {
       // a stalled step leaves its value and width untouched on the device
@@ -557,33 +575,48 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
   return CMC_OK;
 }
 
-// Enqueue one sweep (iteration *d_m + off) for grid.y chains at slot_base.
+// Enqueue one sweep (iteration *d_m + off) for `chains` chains at
+// slot_base.  The gene-phase kernels run on the engine stream; the
+// reduction/hyper tail runs on tail_stream after ev_gene, so the NEXT
+// sweep's eps kernel (which reads only beta and gamma of this sweep) overlaps
+// it, and the next gene kernel waits for ev_tail (it reads nu, tau, theta,
+// sigma).  In a CUDA graph capture the two streams become parallel branches.
 cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
                           long off) {
   cudaError_t r = launch_eps_sweep(p, chains, off, e->stream);
   if (r != cudaSuccess) return r;
+  if ((r = cudaStreamWaitEvent(e->stream, e->ev_tail, 0)) != cudaSuccess) return r;
   if ((r = launch_gene_sweep(p, chains, off, e->stream)) != cudaSuccess) return r;
+  if ((r = cudaEventRecord(e->ev_gene, e->stream)) != cudaSuccess) return r;
+  cudaStream_t t = e->tail_stream;
+  if ((r = cudaStreamWaitEvent(t, e->ev_gene, 0)) != cudaSuccess) return r;
   if (e->world == 1) {
-    if ((r = launch_leaf_a(p, chains, off, e->stream)) != cudaSuccess) return r;
-    if ((r = launch_leaf_b(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
+    if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
   } else {
     const int Q = 2 + (int)e->L;
     const size_t cA = (size_t)e->C * Q * p.leaves_per_rank;
     const size_t cB = (size_t)e->C * e->L * p.leaves_per_rank;
-    if ((r = launch_leaf_a(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
     if (g_nccl.all_gather(e->partA.p + (size_t)e->rank * cA, e->partA.p, cA,
-                          kNcclFloat64, e->comm, e->stream) != 0)
+                          kNcclFloat64, e->comm, t) != 0)
       return cudaErrorUnknown;
-    if ((r = launch_hyper_a(p, chains, off, e->stream)) != cudaSuccess) return r;
-    if ((r = launch_leaf_b(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if ((r = launch_hyper_a(p, chains, off, t)) != cudaSuccess) return r;
+    if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
     if (g_nccl.all_gather(e->partB.p + (size_t)e->rank * cB, e->partB.p, cB,
-                          kNcclFloat64, e->comm, e->stream) != 0)
+                          kNcclFloat64, e->comm, t) != 0)
       return cudaErrorUnknown;
-    if ((r = launch_hyper_b(p, chains, off, e->stream)) != cudaSuccess) return r;
+    if ((r = launch_hyper_b(p, chains, off, t)) != cudaSuccess) return r;
   }
   if (p.monitor_enabled && e->has_ctab && e->ctab.gene_needs_hyper)
-    if ((r = launch_gene_contrast(p, chains, off, e->stream)) != cudaSuccess) return r;
-  return cudaSuccess;
+    if ((r = launch_gene_contrast(p, chains, off, t)) != cudaSuccess) return r;
+  return cudaEventRecord(e->ev_tail, t);
+}
+
+// Join the tail stream back into the engine stream (before the iteration
+// base advances or the host reads results).
+cudaError_t join_tail(cmc_engine* e) {
+  return cudaStreamWaitEvent(e->stream, e->ev_tail, 0);
 }
 
 int set_device_m(cmc_engine* e, long m, cmc_error* err) {
@@ -822,6 +855,9 @@ int cmc_engine_destroy(cmc_engine* e) {
     e->dctab.free_();
     e->d_m.free_();
     if (e->ev0) cudaEventDestroy(e->ev0);
+    if (e->ev_gene) cudaEventDestroy(e->ev_gene);
+    if (e->ev_tail) cudaEventDestroy(e->ev_tail);
+    if (e->tail_stream) cudaStreamDestroy(e->tail_stream);
     if (e->ev1) cudaEventDestroy(e->ev1);
     cudaStreamDestroy(e->stream);
   }
@@ -908,17 +944,22 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
   CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + slot, sizeof(Hyper), cudaMemcpyDeviceToHost));
   const unsigned long long before = hp.clamps;
   hp.err_key = kNoError;
+  hp.err_key_eps = kNoError;
   CUDA_TRY(cudaMemcpy(&e->hyper.p[slot].err_key, &hp.err_key,
+                      sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(&e->hyper.p[slot].err_key_eps, &hp.err_key_eps,
                       sizeof(unsigned long long), cudaMemcpyHostToDevice));
   SweepParams p = e->base;
   p.slot_base = (int)slot;
   p.chain_base = (int)chain;
   p.monitor_enabled = 0;
   CUDA_TRY(enqueue_sweep(e, p, 1, 0));
+  CUDA_TRY(join_tail(e));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + slot, sizeof(Hyper), cudaMemcpyDeviceToHost));
   if (clamps) *clamps += hp.clamps - before;
-  if (hp.err_key != kNoError) return check_stall(e, slot, slot + 1, err);
+  if (hp.err_key != kNoError || hp.err_key_eps != kNoError)
+    return check_stall(e, slot, slot + 1, err);
   return CMC_OK;
 }
 
@@ -975,6 +1016,8 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
       e->graph = nullptr;
       cudaGraph_t g;
       CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+      // fork the tail stream into the capture
+      CUDA_TRY(cudaEventRecord(e->ev_tail, e->stream));
       for (long off = 0; off < chunk; ++off) {
         cudaError_t r = enqueue_sweep(e, p, e->C, off);
         if (r != cudaSuccess) {
@@ -982,6 +1025,7 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
           CUDA_TRY(r);
         }
       }
+      CUDA_TRY(join_tail(e));
       CUDA_TRY(launch_advance(e->d_m.p, chunk, e->stream));
       CUDA_TRY(cudaStreamEndCapture(e->stream, &g));
       CUDA_TRY(cudaGraphInstantiate(&e->graph, g, 0));
@@ -990,10 +1034,17 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
     }
     for (; done + chunk <= total; done += chunk)
       CUDA_TRY(cudaGraphLaunch(e->graph, e->stream));
+    // events recorded inside a capture cannot be waited on outside it:
+    // re-arm them on the real stream (everything so far is stream-ordered)
+    CUDA_TRY(cudaEventRecord(e->ev_tail, e->stream));
+    CUDA_TRY(cudaEventRecord(e->ev_gene, e->stream));
   }
   const long rest = total - done;
   for (long off = 0; off < rest; ++off) CUDA_TRY(enqueue_sweep(e, p, e->C, off));
-  if (rest) CUDA_TRY(launch_advance(e->d_m.p, rest, e->stream));
+  if (rest) {
+    CUDA_TRY(join_tail(e));
+    CUDA_TRY(launch_advance(e->d_m.p, rest, e->stream));
+  }
   CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
   e->timing_pending = true;
   e->host_m = m_end;
@@ -1005,6 +1056,7 @@ int cmc_engine_sync(cmc_engine* e, cmc_error* err) {
   if (!e->dev_ready) return CMC_OK;
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
+  CUDA_TRY(cudaStreamSynchronize(e->tail_stream));
   if (e->timing_pending) {
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));

@@ -49,6 +49,8 @@ struct Hyper {
   double err_x0[2 + kLMax];  // nu, tau, sigma_l
   double err_w[2 + kLMax];
   long long err_m;            // iteration of the recorded stall
+  unsigned long long err_key_eps;  // stall slot of the eps kernel
+  long long err_m_eps;
   unsigned int doneA, doneB;  // last-block counters of the two leaf phases
 };
 

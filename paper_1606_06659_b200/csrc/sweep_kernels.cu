@@ -217,8 +217,15 @@ __device__ __forceinline__ void moments(double* acc, size_t stride, double v,
   acc[3 * stride] = msc;
 }
 
-// Every stall of a chain happens in one iteration (later kernels of a
-// stalled chain return at entry), so err_m is written with one value.
+// Every stall of a chain recorded in one slot happens in one iteration
+// (later kernels of a stalled chain return at entry), so err_m is written
+// with one value.  The eps kernel uses the second slot (err_key_eps): it
+// may overlap the previous iteration's tail; the host reports the record
+// with the smaller (iteration, key).
+__device__ __forceinline__ bool stalled_chain(const Hyper* hp) {
+  return hp->err_key != kNoError || hp->err_key_eps != kNoError;
+}
+
 __device__ __forceinline__ void record_stall(Hyper* hp, unsigned long long key,
                                              long m) {
   atomicMin(&hp->err_key, key);
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   __syncthreads();
   const int slot = p.slot_base + blockIdx.z;
   Hyper* hp = p.hyper + slot;
-  if (hp->err_key != kNoError) return;
+  if (stalled_chain(hp)) return;
   const long gl = (long)blockIdx.x * kGeneBlock + threadIdx.x;
   if (gl >= p.G) return;
   const int n = blockIdx.y;
@@ -323,8 +330,11 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   bool st = false;
   const double x1 = slice_step(f, x0, w, wa, sc, m, rng, st);
   if (st) {
-    // eps and its width stay untouched: the host reads x0 and w back
-    record_stall(hp, stall_key(1, 0, gg, n), m);
+    // eps and its width stay untouched: the host reads x0 and w back.
+    // The eps kernel of iteration m+1 runs concurrently with the tail of
+    // iteration m, so it records into its own slot (see stalled_chain).
+    atomicMin(&hp->err_key_eps, stall_key(1, 0, gg, n));
+    hp->err_m_eps = m;
   } else {
     p.eps[ie] = x1;
     if (tuning) {
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 // evaluations run as one SIMT stream (no early exits: a lane without a
 // gene, or whose gene stalled, idles with alive == false).
 #ifndef CMC_GENE_MIN_BLOCKS
-#define CMC_GENE_MIN_BLOCKS 4
+#define CMC_GENE_MIN_BLOCKS 5
 #endif
 __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
     gene_sweep_kernel(const SweepParams p, const long m_off) {
@@ -354,7 +364,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
   const int tid = threadIdx.x;
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
-  if (hp->err_key != kNoError) return;  // warp-uniform: one load per warp
+  if (stalled_chain(hp)) return;  // warp-uniform: one load per warp
   const long gl_raw = (long)blockIdx.x * kGeneBlock + tid;
   bool alive = gl_raw < p.G;
   const long gl = alive ? gl_raw : 0;
@@ -713,8 +723,7 @@ __device__ void hyper_b_body(const SweepParams& p, int slot, long m) {
     }
   }
   __syncthreads();
-  if (tid == 0 && p.monitor_enabled && m > p.burnin &&
-      hp->err_key == kNoError) {
+  if (tid == 0 && p.monitor_enabled && m > p.burnin && hp->err_key == kNoError) {
     const long cnt = m - p.burnin;
     const double mc = (double)cnt;
     const int K = 2 + 2 * kLMax;
@@ -771,7 +780,7 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned total
 __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
-  if (hp->err_key != kNoError) return;
+  if (stalled_chain(hp)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.L, Q = 2 + L;
   const size_t G = (size_t)p.G, so = (size_t)slot;
@@ -796,7 +805,7 @@ __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
 
 __global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
   const int slot = p.slot_base + blockIdx.x;
-  if (p.hyper[slot].err_key != kNoError) return;
+  if (stalled_chain(p.hyper + slot)) return;
   hyper_a_body(p, slot, *p.d_m + m_off);
 }
 
@@ -804,7 +813,7 @@ __global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
 __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
-  if (hp->err_key != kNoError) return;
+  if (stalled_chain(hp)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.L;
   const size_t G = (size_t)p.G, so = (size_t)slot;
@@ -833,7 +842,7 @@ __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
 
 __global__ void hyper_b_kernel(const SweepParams p, const long m_off) {
   const int slot = p.slot_base + blockIdx.x;
-  if (p.hyper[slot].err_key != kNoError) return;
+  if (stalled_chain(p.hyper + slot)) return;
   hyper_b_body(p, slot, *p.d_m + m_off);
 }
 
@@ -842,7 +851,7 @@ __global__ void hyper_b_kernel(const SweepParams p, const long m_off) {
 __global__ void gene_contrast_kernel(const SweepParams p, const long m_off) {
   const int slot = p.slot_base + blockIdx.y;
   const Hyper* hp = p.hyper + slot;
-  if (hp->err_key != kNoError) return;
+  if (stalled_chain(hp)) return;
   const long gl = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gl >= p.G) return;
   const long m = *p.d_m + m_off;
