@@ -163,6 +163,7 @@ struct cmc_engine {
   int rank = 0, world = 1;
   long g0 = 0, G = 0;  // local range
   nccl_comm comm = nullptr;
+  bool split_tail = false;  // NCCL exchange between the leaf and hyper kernels
   // device
   int device = 0;
   bool dev_ready = false;
@@ -295,7 +296,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.leaves_per_rank = (int)lpr;
   p.world = e->world;
   p.Jmax = e->Jmax;
-  p.fuse_tail = e->world == 1 ? 1 : 0;
+  p.fuse_tail = e->split_tail ? 0 : 1;
   p.y = e->y.p;
   p.A = e->A.p;
   p.X = e->Xd.p;
@@ -590,7 +591,7 @@ cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
   if ((r = cudaEventRecord(e->ev_gene, e->stream)) != cudaSuccess) return r;
   cudaStream_t t = e->tail_stream;
   if ((r = cudaStreamWaitEvent(t, e->ev_gene, 0)) != cudaSuccess) return r;
-  if (e->world == 1) {
+  if (!e->split_tail) {
     if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
   } else {
@@ -1083,7 +1084,7 @@ void* cmc_engine_stream(cmc_engine* e) {
 
 int cmc_engine_launches_per_sweep(const cmc_engine* e) {
   if (!e) return 0;
-  int n = e->world == 1 ? 4 : 6;
+  int n = e->split_tail ? 6 : 4;
   if (e->has_ctab && e->ctab.gene_needs_hyper) ++n;
   return n;
 }
@@ -1110,7 +1111,7 @@ int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
     CUDA_TRY(cudaEventRecord(ev[3 * r + 1], e->stream));
     SweepParams q = p;
     // the tail: everything enqueue_sweep launches after the gene kernel
-    if (e->world == 1) {
+    if (!e->split_tail) {
       CUDA_TRY(launch_leaf_a(q, e->C, r, e->stream));
       CUDA_TRY(launch_leaf_b(q, e->C, r, e->stream));
     } else {
@@ -1246,7 +1247,9 @@ int cmc_engine_shard(cmc_engine* e, int rank, int world, const void* uid,
   e->world = world;
   e->g0 = b;
   e->G = en - b;
-  if (world > 1) {
+  // world == 1 with an id still builds a (1-rank) clique: the exchange path
+  // then runs on one GPU, which is how it is tested without a second GPU
+  if (world > 1 || uid) {
     std::string why;
     if (!g_nccl.load(why)) {
       set_err(err, CMC_ERR_NCCL, why);
@@ -1259,6 +1262,7 @@ int cmc_engine_shard(cmc_engine* e, int rank, int world, const void* uid,
       set_err(err, CMC_ERR_NCCL, "ncclCommInitRank failed");
       return CMC_ERR_NCCL;
     }
+    e->split_tail = true;
   }
   return CMC_OK;
 }
