@@ -171,6 +171,17 @@ struct cmc_engine {
   cudaStream_t tail_stream = nullptr;  // reduction/hyper tail, overlaps the
                                        // next iteration's eps kernel
   cudaEvent_t ev_gene = nullptr, ev_tail = nullptr;
+  // Chain groups ("lanes"): with >= 2 chains the chains are split in two
+  // independent groups on separate stream pairs, so one group's
+  // latency-bound gene kernel co-runs with the other's eps kernel.
+  struct Lane {
+    cudaStream_t s = nullptr, t = nullptr;
+    cudaEvent_t ev_gene = nullptr, ev_tail = nullptr, ev_join = nullptr;
+    int slot0 = 0, chains = 0;
+  };
+  Lane lanes[2];
+  int n_lanes = 1;
+  cudaEvent_t ev_fork = nullptr;
   int C = 1;
   DevBuf<double> y, A, Xd, hd, gval;
   DevBuf<int> goff, gmoff, gmem, saved_slot;
@@ -209,6 +220,28 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaStreamCreateWithFlags(&e->tail_stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_gene, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_tail, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  e->n_lanes = (e->C >= 2 && !e->split_tail) ? 2 : 1;
+  {
+    const int c0 = (int)((e->C + e->n_lanes - 1) / e->n_lanes);
+    for (int k = 0; k < e->n_lanes; ++k) {
+      cmc_engine::Lane& ln = e->lanes[k];
+      ln.slot0 = k * c0;
+      ln.chains = (int)std::min<long>(e->C, (long)(k + 1) * c0) - ln.slot0;
+      if (k == 0) {
+        ln.s = e->stream;
+        ln.t = e->tail_stream;
+        ln.ev_gene = e->ev_gene;
+        ln.ev_tail = e->ev_tail;
+      } else {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ln.s, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ln.t, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ln.ev_gene, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ln.ev_tail, cudaEventDisableTiming));
+      }
+      CUDA_TRY(cudaEventCreateWithFlags(&ln.ev_join, cudaEventDisableTiming));
+    }
+  }
   CUDA_TRY(cudaEventCreate(&e->ev0));
   CUDA_TRY(cudaEventCreate(&e->ev1));
   const long G = e->G, N = e->N, L = e->L, C = e->C;
@@ -582,15 +615,15 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
 // sweep's eps kernel (which reads only beta and gamma of this sweep) overlaps
 // it, and the next gene kernel waits for ev_tail (it reads nu, tau, theta,
 // sigma).  In a CUDA graph capture the two streams become parallel branches.
-cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
-                          long off) {
-  cudaError_t r = launch_eps_sweep(p, chains, off, e->stream);
+cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p, int chains,
+                             long off, cudaStream_t s, cudaStream_t t,
+                             cudaEvent_t ev_gene, cudaEvent_t ev_tail) {
+  cudaError_t r = launch_eps_sweep(p, chains, off, s);
   if (r != cudaSuccess) return r;
-  if ((r = cudaStreamWaitEvent(e->stream, e->ev_tail, 0)) != cudaSuccess) return r;
-  if ((r = launch_gene_sweep(p, chains, off, e->stream)) != cudaSuccess) return r;
-  if ((r = cudaEventRecord(e->ev_gene, e->stream)) != cudaSuccess) return r;
-  cudaStream_t t = e->tail_stream;
-  if ((r = cudaStreamWaitEvent(t, e->ev_gene, 0)) != cudaSuccess) return r;
+  if ((r = cudaStreamWaitEvent(s, ev_tail, 0)) != cudaSuccess) return r;
+  if ((r = launch_gene_sweep(p, chains, off, s)) != cudaSuccess) return r;
+  if ((r = cudaEventRecord(ev_gene, s)) != cudaSuccess) return r;
+  if ((r = cudaStreamWaitEvent(t, ev_gene, 0)) != cudaSuccess) return r;
   if (!e->split_tail) {
     if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
@@ -611,13 +644,58 @@ cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
   }
   if (p.monitor_enabled && e->has_ctab && e->ctab.gene_needs_hyper)
     if ((r = launch_gene_contrast(p, chains, off, t)) != cudaSuccess) return r;
-  return cudaEventRecord(e->ev_tail, t);
+  return cudaEventRecord(ev_tail, t);
+}
+
+// One sweep of chains [slot_base, slot_base + chains) on lane 0.
+cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
+                          long off) {
+  return enqueue_sweep_on(e, p, chains, off, e->stream, e->tail_stream, e->ev_gene,
+                          e->ev_tail);
 }
 
 // Join the tail stream back into the engine stream (before the iteration
 // base advances or the host reads results).
 cudaError_t join_tail(cmc_engine* e) {
   return cudaStreamWaitEvent(e->stream, e->ev_tail, 0);
+}
+
+// Fork lanes 1.. off the engine stream (inside or outside a capture).
+cudaError_t fork_lanes(cmc_engine* e) {
+  cudaError_t r = cudaEventRecord(e->ev_fork, e->stream);
+  if (r != cudaSuccess) return r;
+  for (int k = 1; k < e->n_lanes; ++k) {
+    cmc_engine::Lane& ln = e->lanes[k];
+    if ((r = cudaStreamWaitEvent(ln.s, e->ev_fork, 0)) != cudaSuccess) return r;
+    if ((r = cudaEventRecord(ln.ev_tail, ln.s)) != cudaSuccess) return r;
+  }
+  return cudaEventRecord(e->ev_tail, e->stream);
+}
+
+// Every lane's sweep of iteration *d_m + off.
+cudaError_t enqueue_all_lanes(cmc_engine* e, const SweepParams& base, long off) {
+  for (int k = 0; k < e->n_lanes; ++k) {
+    cmc_engine::Lane& ln = e->lanes[k];
+    SweepParams p = base;
+    p.slot_base = ln.slot0;
+    p.chain_base = ln.slot0;
+    cudaError_t r = enqueue_sweep_on(e, p, ln.chains, off, ln.s, ln.t, ln.ev_gene, ln.ev_tail);
+    if (r != cudaSuccess) return r;
+  }
+  return cudaSuccess;
+}
+
+// Join every lane's streams back into the engine stream.
+cudaError_t join_lanes(cmc_engine* e) {
+  for (int k = 0; k < e->n_lanes; ++k) {
+    cmc_engine::Lane& ln = e->lanes[k];
+    cudaError_t r = cudaStreamWaitEvent(ln.s, ln.ev_tail, 0);
+    if (r != cudaSuccess) return r;
+    if (k == 0) continue;
+    if ((r = cudaEventRecord(ln.ev_join, ln.s)) != cudaSuccess) return r;
+    if ((r = cudaStreamWaitEvent(e->stream, ln.ev_join, 0)) != cudaSuccess) return r;
+  }
+  return cudaSuccess;
 }
 
 int set_device_m(cmc_engine* e, long m, cmc_error* err) {
@@ -856,6 +934,18 @@ int cmc_engine_destroy(cmc_engine* e) {
     e->dctab.free_();
     e->d_m.free_();
     if (e->ev0) cudaEventDestroy(e->ev0);
+    for (int k = 1; k < e->n_lanes; ++k) {
+      cmc_engine::Lane& ln = e->lanes[k];
+      cudaStreamSynchronize(ln.s);
+      cudaStreamSynchronize(ln.t);
+      cudaEventDestroy(ln.ev_gene);
+      cudaEventDestroy(ln.ev_tail);
+      cudaStreamDestroy(ln.s);
+      cudaStreamDestroy(ln.t);
+    }
+    for (int k = 0; k < e->n_lanes; ++k)
+      if (e->lanes[k].ev_join) cudaEventDestroy(e->lanes[k].ev_join);
+    if (e->ev_fork) cudaEventDestroy(e->ev_fork);
     if (e->ev_gene) cudaEventDestroy(e->ev_gene);
     if (e->ev_tail) cudaEventDestroy(e->ev_tail);
     if (e->tail_stream) cudaStreamDestroy(e->tail_stream);
@@ -1017,33 +1107,33 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
       e->graph = nullptr;
       cudaGraph_t g;
       CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-      // fork the tail stream into the capture
-      CUDA_TRY(cudaEventRecord(e->ev_tail, e->stream));
-      for (long off = 0; off < chunk; ++off) {
-        cudaError_t r = enqueue_sweep(e, p, e->C, off);
-        if (r != cudaSuccess) {
-          cudaStreamEndCapture(e->stream, &g);
-          CUDA_TRY(r);
-        }
-      }
-      CUDA_TRY(join_tail(e));
-      CUDA_TRY(launch_advance(e->d_m.p, chunk, e->stream));
-      CUDA_TRY(cudaStreamEndCapture(e->stream, &g));
+      // fork the other lanes and the tail streams into the capture
+      cudaError_t r = fork_lanes(e);
+      for (long off = 0; r == cudaSuccess && off < chunk; ++off)
+        r = enqueue_all_lanes(e, p, off);
+      if (r == cudaSuccess) r = join_lanes(e);
+      if (r == cudaSuccess) r = launch_advance(e->d_m.p, chunk, e->stream);
+      cudaError_t r2 = cudaStreamEndCapture(e->stream, &g);
+      CUDA_TRY(r);
+      CUDA_TRY(r2);
       CUDA_TRY(cudaGraphInstantiate(&e->graph, g, 0));
       cudaGraphDestroy(g);
       e->graph_len = chunk;
     }
     for (; done + chunk <= total; done += chunk)
       CUDA_TRY(cudaGraphLaunch(e->graph, e->stream));
-    // events recorded inside a capture cannot be waited on outside it:
-    // re-arm them on the real stream (everything so far is stream-ordered)
-    CUDA_TRY(cudaEventRecord(e->ev_tail, e->stream));
-    CUDA_TRY(cudaEventRecord(e->ev_gene, e->stream));
+    // events recorded inside the capture cannot be waited on outside it:
+    // re-arm them on the real streams (all work so far is stream-ordered)
+    CUDA_TRY(fork_lanes(e));
+    CUDA_TRY(join_lanes(e));
   }
   const long rest = total - done;
-  for (long off = 0; off < rest; ++off) CUDA_TRY(enqueue_sweep(e, p, e->C, off));
   if (rest) {
-    CUDA_TRY(join_tail(e));
+    // events recorded inside a capture cannot be waited on outside it:
+    // fork_lanes re-arms every event on the real streams
+    CUDA_TRY(fork_lanes(e));
+    for (long off = 0; off < rest; ++off) CUDA_TRY(enqueue_all_lanes(e, p, off));
+    CUDA_TRY(join_lanes(e));
     CUDA_TRY(launch_advance(e->d_m.p, rest, e->stream));
   }
   CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
@@ -1058,6 +1148,10 @@ int cmc_engine_sync(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   CUDA_TRY(cudaStreamSynchronize(e->tail_stream));
+  for (int k = 1; k < e->n_lanes; ++k) {
+    CUDA_TRY(cudaStreamSynchronize(e->lanes[k].s));
+    CUDA_TRY(cudaStreamSynchronize(e->lanes[k].t));
+  }
   if (e->timing_pending) {
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
