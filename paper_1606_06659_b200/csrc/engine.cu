@@ -179,7 +179,7 @@ struct cmc_engine {
     cudaEvent_t ev_gene = nullptr, ev_tail = nullptr, ev_join = nullptr;
     int slot0 = 0, chains = 0;
   };
-  Lane lanes[2];
+  Lane lanes[4];
   int n_lanes = 1;
   cudaEvent_t ev_fork = nullptr;
   int C = 1;
@@ -221,13 +221,15 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_gene, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_tail, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
-  e->n_lanes = (e->C >= 2 && !e->split_tail) ? 2 : 1;
+#ifndef CMC_MAX_LANES
+#define CMC_MAX_LANES 2
+#endif
+  e->n_lanes = e->split_tail ? 1 : (int)std::min<long>(e->C, CMC_MAX_LANES);
   {
-    const int c0 = (int)((e->C + e->n_lanes - 1) / e->n_lanes);
     for (int k = 0; k < e->n_lanes; ++k) {
       cmc_engine::Lane& ln = e->lanes[k];
-      ln.slot0 = k * c0;
-      ln.chains = (int)std::min<long>(e->C, (long)(k + 1) * c0) - ln.slot0;
+      ln.slot0 = (int)(k * e->C / e->n_lanes);
+      ln.chains = (int)((k + 1) * e->C / e->n_lanes) - ln.slot0;
       if (k == 0) {
         ln.s = e->stream;
         ln.t = e->tail_stream;
