@@ -12,6 +12,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/countmc_b200.h"
@@ -124,6 +125,27 @@ long matrix_rank(std::vector<double> A, long n, long m, double tol) {
     ++rank;
   }
   return rank;
+}
+
+// Host fork-join over [0, n) in contiguous chunks (setup and transposes
+// only; every element is computed independently, so results do not depend
+// on the thread count).
+template <class F>
+void host_parallel_for(long n, F&& body) {
+  unsigned hw = std::thread::hardware_concurrency();
+  const long nt = std::max<long>(1, std::min<long>(hw ? hw : 1, n / 4096));
+  if (nt <= 1) {
+    body(0L, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const long chunk = (n + nt - 1) / nt;
+  for (long t = 0; t < nt; ++t) {
+    const long lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo >= hi) break;
+    th.emplace_back([&body, lo, hi] { body(lo, hi); });
+  }
+  for (auto& x : th) x.join();
 }
 
 template <class T>
@@ -414,12 +436,14 @@ void initial_state_host(const cmc_engine* e, long chain, double* st) {
   double hbar = 0.0;
   for (double v : e->h) hbar += v;
   hbar /= (double)N;
-  for (long g = 0; g < G; ++g) {
-    double mean = 0.0;
-    for (long n = 0; n < N; ++n) mean += (double)e->counts[(size_t)g * N + n];
-    mean /= (double)N;
-    beta[g * L] = std::log(mean + 1.0) - hbar;
-  }
+  host_parallel_for(G, [&](long g0, long g1) {
+    for (long g = g0; g < g1; ++g) {
+      double mean = 0.0;
+      for (long n = 0; n < N; ++n) mean += (double)e->counts[(size_t)g * N + n];
+      mean /= (double)N;
+      beta[g * L] = std::log(mean + 1.0) - hbar;
+    }
+  });
   double tbar = 0.0;
   for (long g = 0; g < G; ++g) tbar += beta[g * L];
   theta[0] = tbar / (double)G;
@@ -433,11 +457,13 @@ void initial_state_host(const cmc_engine* e, long chain, double* st) {
     auto clamp_interior = [](double v, double lo, double hi) {
       return std::min(std::max(v, lo), hi);
     };
-    for (long g = 0; g < G; ++g) {
-      for (long n = 0; n < N; ++n) eps[g * N + n] += z(kSiteEps, (uint64_t)(g * N + n));
-      gam[g] = std::max(1e-3, gam[g] + z(kSiteGamma, (uint64_t)g));
-      for (long l = 0; l < L; ++l) beta[g * L + l] += z(kSiteBeta, (uint64_t)(g * L + l));
-    }
+    host_parallel_for(G, [&](long g0, long g1) {
+      for (long g = g0; g < g1; ++g) {
+        for (long n = 0; n < N; ++n) eps[g * N + n] += z(kSiteEps, (uint64_t)(g * N + n));
+        gam[g] = std::max(1e-3, gam[g] + z(kSiteGamma, (uint64_t)g));
+        for (long l = 0; l < L; ++l) beta[g * L + l] += z(kSiteBeta, (uint64_t)(g * L + l));
+      }
+    });
     for (long l = 0; l < L; ++l) {
       theta[l] += z(kSiteTheta, (uint64_t)l);
       const double sv = e->s[l];
@@ -460,8 +486,10 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
   const double* sigma = theta + L;
   std::vector<double> buf((size_t)std::max(N, L) * G);
   auto put_gn = [&](const double* src, double* dst, long K) -> cudaError_t {
-    for (long k = 0; k < K; ++k)
-      for (long g = 0; g < G; ++g) buf[(size_t)k * G + g] = src[(g0 + g) * K + k];
+    host_parallel_for(G, [&](long a, long b) {
+      for (long g = a; g < b; ++g)
+        for (long k = 0; k < K; ++k) buf[(size_t)k * G + g] = src[(g0 + g) * K + k];
+    });
     return cudaMemcpy(dst, buf.data(), sizeof(double) * K * G, cudaMemcpyHostToDevice);
   };
   const size_t so = (size_t)c;
@@ -516,8 +544,10 @@ int download_state(cmc_engine* e, long c, double* st, double* tw, double* ta,
     cudaError_t r = cudaMemcpy(buf.data(), src, sizeof(double) * K * G,
                                cudaMemcpyDeviceToHost);
     if (r != cudaSuccess) return r;
-    for (long k = 0; k < K; ++k)
-      for (long g = 0; g < G; ++g) dst[(g0 + g) * K + k] = buf[(size_t)k * G + g];
+    host_parallel_for(G, [&](long a, long b) {
+      for (long g = a; g < b; ++g)
+        for (long k = 0; k < K; ++k) dst[(g0 + g) * K + k] = buf[(size_t)k * G + g];
+    });
     return cudaSuccess;
   };
   const size_t so = (size_t)c;
@@ -1265,8 +1295,10 @@ int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,
     buf.resize((size_t)L * G);
     CUDA_TRY(cudaMemcpy(buf.data(), e->acc_beta.p + so * 4 * L * G + (size_t)k * L * G,
                         sizeof(double) * L * G, cudaMemcpyDeviceToHost));
-    for (long g = 0; g < G; ++g)
-      for (long l = 0; l < L; ++l) dst[i + (g0 + g) * L + l] = buf[(size_t)l * G + g];
+    host_parallel_for(G, [&](long a, long b) {
+      for (long g = a; g < b; ++g)
+        for (long l = 0; l < L; ++l) dst[i + (g0 + g) * L + l] = buf[(size_t)l * G + g];
+    });
     i += Gt * L;
     buf.resize((size_t)G);
     CUDA_TRY(cudaMemcpy(buf.data(), e->acc_gam.p + so * 4 * G + (size_t)k * G,
@@ -1276,8 +1308,10 @@ int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,
     buf.resize((size_t)N * G);
     CUDA_TRY(cudaMemcpy(buf.data(), e->acc_eps.p + so * 4 * N * G + (size_t)k * N * G,
                         sizeof(double) * N * G, cudaMemcpyDeviceToHost));
-    for (long g = 0; g < G; ++g)
-      for (long n = 0; n < N; ++n) dst[i + (g0 + g) * N + n] = buf[(size_t)n * G + g];
+    host_parallel_for(G, [&](long a, long b) {
+      for (long g = a; g < b; ++g)
+        for (long n = 0; n < N; ++n) dst[i + (g0 + g) * N + n] = buf[(size_t)n * G + g];
+    });
   }
   if (e->has_ctab) {
     if (o->contrast_prob)
