@@ -287,6 +287,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(e->A.alloc((size_t)L * G));
   CUDA_TRY(launch_compute_A(e->y.p, e->Xd.p, e->A.p, (int)G, (int)N, (int)L,
                             e->stream));
+  CUDA_TRY(launch_fastmath_setup(e->stream));
   CUDA_TRY(e->goff.alloc(e->grp_off.size()));
   CUDA_TRY(cudaMemcpy(e->goff.p, e->grp_off.data(), sizeof(int) * e->grp_off.size(),
                       cudaMemcpyHostToDevice));

@@ -23,13 +23,18 @@ __constant__ double kExpC[8] = {
     1.4841640746974334e-08,   // ln2/32, low part
     1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
 
-struct ExpTable {
-  double t[32];  // 2^(j/32), correctly rounded
-};
+// 2^(j/32) computed once per process by fastmath_setup_kernel (global)
+// and copied into each block's shared table at kernel start (one coalesced
+// load per thread instead of an exp2 per entry).
+__device__ double g_exp_table[32];
+
+__global__ void fastmath_setup_kernel() {
+  if (threadIdx.x < 32) g_exp_table[threadIdx.x] = exp2((double)threadIdx.x / 32.0);
+}
 
 // Fill a block-shared table (call with all threads, then __syncthreads()).
 __device__ __forceinline__ void exp_table_init(double* tab) {
-  if (threadIdx.x < 32) tab[threadIdx.x] = exp2((double)threadIdx.x / 32.0);
+  if (threadIdx.x < 32) tab[threadIdx.x] = g_exp_table[threadIdx.x];
 }
 
 __device__ __forceinline__ double fast_exp(double x, const double* tab) {

@@ -945,6 +945,11 @@ cudaError_t launch_gene_contrast(const SweepParams& p, int chains, long m_off,
   return cudaGetLastError();
 }
 
+cudaError_t launch_fastmath_setup(cudaStream_t s) {
+  fastmath_setup_kernel<<<1, 32, 0, s>>>();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_advance(long* d_m, long by, cudaStream_t s) {
   advance_kernel<<<1, 1, 0, s>>>(d_m, by);
   return cudaGetLastError();
