@@ -207,6 +207,11 @@ int cmc_engine_launches_per_sweep(const cmc_engine* engine);
 int cmc_engine_profile(cmc_engine* engine, long m_begin, long reps,
                        double* gene_ms, double* tail_ms, cmc_error* err);
 
+/* Profiling aid: warp-level timeline {kernel<<56|slot<<48|smid<<32|block,
+ * t_start_ns, t_end_ns} of the next `sweeps` sweeps (direct launches). */
+int cmc_engine_trace(cmc_engine* engine, long m_begin, long sweeps,
+                     unsigned long long* out, long cap, long* n_out, cmc_error* err);
+
 /* ChainOutput of one chain after run()/sweeps(); see cmc_output_view. */
 int cmc_engine_get_output(cmc_engine* engine, long chain,
                           const cmc_output_view* out, cmc_error* err);

@@ -411,6 +411,14 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.partA = e->partA.p;
   p.partB = e->partB.p;
   p.C = (int)C;
+  {
+    int least = 0, greatest = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    p.prio_eps = least;
+    p.prio_tail = greatest;
+    p.prio_gene = least + (greatest - least) / 2;
+    if (p.prio_gene == least && greatest != least) p.prio_gene = greatest;
+  }
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->dev_ready = true;
   return CMC_OK;
@@ -1149,7 +1157,7 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
       cudaError_t r2 = cudaStreamEndCapture(e->stream, &g);
       CUDA_TRY(r);
       CUDA_TRY(r2);
-      CUDA_TRY(cudaGraphInstantiate(&e->graph, g, 0));
+      CUDA_TRY(cudaGraphInstantiate(&e->graph, g, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(g);
       e->graph_len = chunk;
     }
@@ -1264,6 +1272,43 @@ int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
   if (gene_ms) *gene_ms = g / reps;
   if (tail_ms) *tail_ms = t / reps;
   return check_stall(e, 0, e->C, err);
+}
+
+// Debug timeline: record warp start/end times of the next `sweeps` sweeps
+// (direct launches on the lanes, no graph); returns the record count.
+int cmc_engine_trace(cmc_engine* e, long m_begin, long sweeps, unsigned long long* out,
+                     long cap, long* n_out, cmc_error* err) {
+  if (!e || !e->begun || sweeps < 1) {
+    set_err(err, CMC_ERR_ARG, "trace needs begin()");
+    return CMC_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(e->device));
+  int rc = set_device_m(e, m_begin, err);
+  if (rc) return rc;
+  unsigned long long* d_tr = nullptr;
+  unsigned int* d_n = nullptr;
+  CUDA_TRY(cudaMalloc(&d_tr, sizeof(unsigned long long) * 3 * cap));
+  CUDA_TRY(cudaMalloc(&d_n, sizeof(unsigned int)));
+  CUDA_TRY(cudaMemset(d_n, 0, sizeof(unsigned int)));
+  SweepParams p = e->base;
+  p.monitor_enabled = 1;
+  p.trace = d_tr;
+  p.trace_n = d_n;
+  p.trace_cap = (unsigned)cap;
+  CUDA_TRY(fork_lanes(e));
+  for (long off = 0; off < sweeps; ++off) CUDA_TRY(enqueue_all_lanes(e, p, off));
+  CUDA_TRY(join_lanes(e));
+  CUDA_TRY(launch_advance(e->d_m.p, sweeps, e->stream));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->host_m = m_begin + sweeps;
+  unsigned int n = 0;
+  CUDA_TRY(cudaMemcpy(&n, d_n, sizeof(n), cudaMemcpyDeviceToHost));
+  n = std::min<unsigned>(n, (unsigned)cap);
+  CUDA_TRY(cudaMemcpy(out, d_tr, sizeof(unsigned long long) * 3 * n, cudaMemcpyDeviceToHost));
+  *n_out = n;
+  cudaFree(d_tr);
+  cudaFree(d_n);
+  return CMC_OK;
 }
 
 int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,

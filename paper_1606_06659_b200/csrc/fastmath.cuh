@@ -37,8 +37,8 @@ __device__ __forceinline__ void exp_table_init(double* tab) {
   if (threadIdx.x < 32) tab[threadIdx.x] = g_exp_table[threadIdx.x];
 }
 
-__device__ __forceinline__ double fast_exp(double x, const double* tab) {
-  if (!(x >= -707.0 && x <= 700.0)) return exp(x);
+__device__ __forceinline__ double fast_exp_le700(double x, const double* tab) {
+  if (x < -707.0) return exp(x);
   const double t = fma(x, kExpC[0], kExpC[1]);
   const int k = __double2loint(t);
   const double kd = t - kExpC[1];
@@ -52,6 +52,11 @@ __device__ __forceinline__ double fast_exp(double x, const double* tab) {
   const double tj = tab[k & 31];
   const double res = fma(tj, p, tj);
   return __hiloint2double(__double2hiint(res) + ((k >> 5) << 20), __double2loint(res));
+}
+
+__device__ __forceinline__ double fast_exp(double x, const double* tab) {
+  if (x > 700.0) return exp(x);
+  return fast_exp_le700(x, tab);
 }
 
 }  // namespace cmc

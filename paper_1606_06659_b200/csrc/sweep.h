@@ -118,6 +118,14 @@ struct SweepParams {
   double* partA;  // [world][C][2+L][leaves_per_rank]
   double* partB;  // [world][C][L][leaves_per_rank]
   int C;          // chains resident (stride of the partial buffers)
+  // optional block timeline (debug/profiling): per record {kernel<<56 |
+  // slot<<48 | smid<<32 | blockIdx.x, t_start_ns, t_end_ns}
+  unsigned long long* trace;
+  unsigned int* trace_n;
+  unsigned int trace_cap;
+  // launch priorities (host side): the tail and gene kernels are on the
+  // critical path, the next sweep's eps kernel is not
+  int prio_eps, prio_gene, prio_tail;
 };
 
 // Launch wrappers (sweep_kernels.cu).  `chains` = grid.y.

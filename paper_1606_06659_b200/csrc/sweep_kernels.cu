@@ -114,20 +114,106 @@ __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
   return x1;
 }
 
+// Two-phase slice step for log densities whose exp terms are exp(v x + c):
+// the step-out evaluation points move by exactly -w (left) / +w (right)
+// and the step-out draws no random numbers, so (1) both sides step out in
+// the same trip -- the reference runs left then right, but each side's
+// stopping rule depends only on its own evaluations -- and (2) each side
+// carries exp(v x + c) multiplicatively (times exp(-/+ v w)) instead of
+// recomputing it.  The evaluation points lo, hi themselves are updated
+// exactly as the reference does (lo -= w, hi += w), so the slice result is
+// unchanged; the multiplicative exp differs from a fresh exp in the last
+// bits only, which decides comparisons like libm differences do.  Clamp
+// events are counted only for evaluations the reference performs.  The
+// shrinkage phase uses the full density.  F provides operator() (full),
+// side_init(lo, hi, w), eval_l/eval_r(x, counted) and step_l/step_r().
+template <class F>
+__device__ __forceinline__ double slice_step_so2(F& f, double x0, double& w,
+                                                 double& wa, const SliceCfg& sc,
+                                                 long m, Stream& rng,
+                                                 bool& stalled) {
+  const double fx0 = f(x0);
+  const double logu = fx0 + log(rng.u01());
+  const double wv = w;
+  double lo = x0 - wv * rng.u01();
+  double hi = lo + wv;
+  const int kl0 = (int)rng.uniform_int_pre((uint64_t)sc.K + 1, sc.reject_below, sc.inv);
+  int kl = kl0, kr = sc.K - kl0;
+  bool goL = kl > 0, goR = kr > 0;
+  f.side_init(lo, hi, wv);
+  while (goL || goR) {
+    const double fl = f.eval_l(lo, goL);
+    const double fr = f.eval_r(hi, goR);
+    const bool inL = goL && logu < fl;
+    const bool inR = goR && logu < fr;
+    if (inL) {
+      lo -= wv;
+      f.step_l();
+    }
+    if (inR) {
+      hi += wv;
+      f.step_r();
+    }
+    kl -= inL ? 1 : 0;
+    kr -= inR ? 1 : 0;
+    goL = inL && kl > 0;
+    goR = inR && kr > 0;
+  }
+  for (int it = 0;;) {
+    const double xs = lo + (hi - lo) * rng.u01();
+    if (f(xs) > logu) {
+      if (m <= sc.burnin) tune_update(w, wa, m, fabs(xs - x0), sc.tune_cutoff);
+      return xs;
+    }
+    if (xs > x0)
+      hi = xs;
+    else
+      lo = xs;
+    if (++it >= sc.max_shrink) {
+      stalled = true;
+      return x0;
+    }
+  }
+}
+
 // log full conditional of eps_gn, P:src/model.cpp:70-74 (clamped_exp
 // :13-19): y*e - exp(min(h + eta + e, 700)) - e*e / (2 gamma).
 struct EpsF {
-  double y, cn, inv_two_gam;
+  double y, cn, inv_two_gam, e700;
   const double* tab;
   unsigned clamps;
+  double EL, ER, rL, rR;  // step-out: exp(cn + lo), exp(cn + hi), exp(-w), exp(w)
   __device__ __forceinline__ double operator()(double x) {
-    double t = cn + x;
+    const double t = cn + x;
+    double e;
     if (t > kExpClamp) {
       ++clamps;
-      t = kExpClamp;
+      e = e700;
+    } else {
+      e = fast_exp_le700(t, tab);
     }
-    return y * x - fast_exp(t, tab) - x * x * inv_two_gam;
+    return y * x - e - x * x * inv_two_gam;
   }
+  __device__ __forceinline__ void side_init(double lo, double hi, double w) {
+    const double tl = cn + lo, th = cn + hi;
+    EL = tl > kExpClamp ? 0.0 : fast_exp_le700(tl, tab);
+    ER = th > kExpClamp ? 0.0 : fast_exp_le700(th, tab);
+    rR = fast_exp_le700(w, tab);
+    rL = 1.0 / rR;
+  }
+  // value at x with the carried exp E (recomputed if it left the normal
+  // range, e.g. after a clamp or an underflow)
+  __device__ __forceinline__ double side_eval(double x, double& E, bool counted) {
+    const double t = cn + x;
+    const bool cl = t > kExpClamp;
+    if (!cl && !(E > 1e-290 && E < 1e290)) E = fast_exp_le700(t, tab);
+    clamps += (cl && counted) ? 1u : 0u;
+    return y * x - (cl ? e700 : E) - x * x * inv_two_gam;
+  }
+  __device__ __forceinline__ double eval_l(double x, bool c) { return side_eval(x, EL, c); }
+  __device__ __forceinline__ double eval_r(double x, bool c) { return side_eval(x, ER, c); }
+  __device__ __forceinline__ void step_l() { EL *= rL; }
+  __device__ __forceinline__ void step_r() { ER *= rR; }
 };
 
 // log inverse-gamma, P:src/model.cpp:84-87
@@ -192,6 +278,41 @@ struct BetaF {
     }
     const double zz = b - theta;
     return tot - zz * zz * inv_two_sig2;
+  }
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Warp timeline record (only when p.trace is set): lane 0 opens a record
+// {kernel<<56 | slot<<48 | smid<<32 | blockIdx.x, t_start, t_end} at kernel
+// entry, and every lane raises t_end when it leaves (destructor, so every
+// return path is covered).
+struct WarpTrace {
+  unsigned long long* rec;
+  __device__ __forceinline__ WarpTrace(const SweepParams& p, int kernel, int slot) : rec(nullptr) {
+    if (!p.trace) return;
+    unsigned i = 0;
+    if ((threadIdx.x & 31) == 0) {
+      i = atomicAdd(p.trace_n, 1u);
+      if (i < p.trace_cap) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[3 * i] = ((unsigned long long)kernel << 56) |
+                         ((unsigned long long)slot << 48) |
+                         ((unsigned long long)smid << 32) | blockIdx.x;
+        p.trace[3 * i + 1] = gtimer();
+        p.trace[3 * i + 2] = 0;
+      }
+    }
+    i = __shfl_sync(__activemask(), i, 0);
+    if (i < p.trace_cap) rec = p.trace + 3 * i;
+  }
+  __device__ __forceinline__ ~WarpTrace() {
+    if (rec) atomicMax(rec + 2, gtimer());
   }
 };
 
@@ -299,6 +420,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   __shared__ double exp_tab[32];
   exp_table_init(exp_tab);
   __syncthreads();
+  WarpTrace wt(p, 1, p.slot_base + blockIdx.z);
   const int slot = p.slot_base + blockIdx.z;
   Hyper* hp = p.hyper + slot;
   if (stalled_chain(hp)) return;
@@ -321,14 +443,14 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   double xb = 0.0;
   for (int l = 0; l < L; ++l) xb += __ldg(p.X + n * L + l) * beta[(size_t)l * G + gl];
   const double inv_two_gam = 1.0 / (2.0 * p.gam[so * G + gl]);
-  EpsF f{__ldg(p.y + i), __ldg(p.h + n) + xb, inv_two_gam, exp_tab, 0u};
+  EpsF f{__ldg(p.y + i), __ldg(p.h + n) + xb, inv_two_gam, p.exp_clamp, exp_tab, 0u};
   const double x0 = p.eps[ie];
   double w = p.eps_w[ie];
   double wa = tuning ? p.eps_wa[ie] : 0.0;
   Stream rng;
   rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
   bool st = false;
-  const double x1 = slice_step(f, x0, w, wa, sc, m, rng, st);
+  const double x1 = slice_step_so2(f, x0, w, wa, sc, m, rng, st);
   if (st) {
     // eps and its width stay untouched: the host reads x0 and w back.
     // The eps kernel of iteration m+1 runs concurrently with the tail of
@@ -361,6 +483,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
   __shared__ double exp_tab[32];
   exp_table_init(exp_tab);
   __syncthreads();
+  WarpTrace wt(p, 2, p.slot_base + blockIdx.y);
   const int tid = threadIdx.x;
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
@@ -778,6 +901,7 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned total
 // Leaf sums of log gamma (q=0), 1/gamma (q=1), beta_l (q=2+l); one warp
 // per quantity, one block per local leaf.
 __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
+  WarpTrace wt(p, 3, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
   if (stalled_chain(hp)) return;
@@ -811,6 +935,7 @@ __global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
 
 // Leaf sums of (beta_l - theta_l)^2 with theta of this iteration.
 __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
+  WarpTrace wt(p, 4, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
   if (stalled_chain(hp)) return;
@@ -883,6 +1008,24 @@ __global__ void compute_A_kernel(const double* y, const double* X, double* A,
 
 }  // namespace
 
+// Launch with a scheduling priority (cudaLaunchAttributePriority; kept by
+// graph capture, honoured with cudaGraphInstantiateFlagUseNodePriority).
+template <class K>
+cudaError_t launch_prio(K kernel, dim3 grid, dim3 block, size_t smem,
+                        cudaStream_t s, int prio, const SweepParams& p, long m_off) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = prio;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, p, m_off);
+}
+
 int gene_sweep_smem_bytes(int N, int Jmax) {
   return (int)(sizeof(double) * (size_t)(N + 2 * Jmax) * kGeneBlock);
 }
@@ -890,8 +1033,7 @@ int gene_sweep_smem_bytes(int N, int Jmax) {
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
                              cudaStream_t s) {
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)p.N, (unsigned)chains);
-  eps_sweep_kernel<<<grid, kGeneBlock, 0, s>>>(p, m_off);
-  return cudaGetLastError();
+  return launch_prio(eps_sweep_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_eps, p, m_off);
 }
 
 cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
@@ -905,8 +1047,7 @@ cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
     configured = smem;
   }
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)chains);
-  gene_sweep_kernel<<<grid, kGeneBlock, smem, s>>>(p, m_off);
-  return cudaGetLastError();
+  return launch_prio(gene_sweep_kernel, grid, dim3(kGeneBlock), smem, s, p.prio_gene, p, m_off);
 }
 
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
@@ -914,35 +1055,30 @@ cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
   const int Q = 2 + p.L;
   const int threads = 32 * (Q > 2 ? Q : 2);
   dim3 grid((unsigned)p.n_leaves_local, (unsigned)chains);
-  leaf_a_kernel<<<grid, threads < 64 ? 64 : threads, 0, s>>>(p, m_off);
-  return cudaGetLastError();
+  return launch_prio(leaf_a_kernel, grid, dim3(threads < 64 ? 64 : threads), 0, s, p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_hyper_a(const SweepParams& p, int chains, long m_off,
                            cudaStream_t s) {
-  hyper_a_kernel<<<chains, 32 * (2 + p.L), 0, s>>>(p, m_off);
-  return cudaGetLastError();
+  return launch_prio(hyper_a_kernel, dim3(chains), dim3(32 * (2 + p.L)), 0, s, p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_leaf_b(const SweepParams& p, int chains, long m_off,
                           cudaStream_t s) {
   const int threads = 32 * (p.L > 1 ? p.L : 1);
   dim3 grid((unsigned)p.n_leaves_local, (unsigned)chains);
-  leaf_b_kernel<<<grid, threads < 32 ? 32 : threads, 0, s>>>(p, m_off);
-  return cudaGetLastError();
+  return launch_prio(leaf_b_kernel, grid, dim3(threads < 32 ? 32 : threads), 0, s, p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_hyper_b(const SweepParams& p, int chains, long m_off,
                            cudaStream_t s) {
-  hyper_b_kernel<<<chains, 32 * p.L, 0, s>>>(p, m_off);
-  return cudaGetLastError();
+  return launch_prio(hyper_b_kernel, dim3(chains), dim3(32 * p.L), 0, s, p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_gene_contrast(const SweepParams& p, int chains, long m_off,
                                  cudaStream_t s) {
   dim3 grid((unsigned)((p.G + 255) / 256), (unsigned)chains);
-  gene_contrast_kernel<<<grid, 256, 0, s>>>(p, m_off);
-  return cudaGetLastError();
+  return launch_prio(gene_contrast_kernel, grid, dim3(256), 0, s, p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_fastmath_setup(cudaStream_t s) {
