@@ -207,6 +207,30 @@ int cmc_engine_launches_per_sweep(const cmc_engine* engine);
 int cmc_engine_profile(cmc_engine* engine, long m_begin, long reps,
                        double* gene_ms, double* tail_ms, cmc_error* err);
 
+/* Post-run diagnostics (reference build_diagnostics, src/io.cpp:507-569,
+ * over src/diagnostics.cpp), computed on the device from the resident
+ * accumulators after run()/sweeps(): one row per parameter in ChainOutput
+ * order [nu | tau | theta L | sigma L | beta G x L | gamma G]
+ * (R = 2 + 2L + G(L+1) rows): Gelman-Rubin rhat, the pooled mean and sd
+ * and the normal-approximation 95% interval (pool_moments /
+ * credible_interval); flags bit0 = degenerate (W = 0), bit1 = pass
+ * (rhat < 1.1 or degenerate), bit2 = accumulator corruption.  ESS
+ * (Geyer initial positive sequence) for every retained thinned column, in
+ * sample order; ess_status 0 ok, 1 undefined (< 4 rows), 2 degenerate.
+ * Needs >= 2 chains (ConfigError otherwise, as gelman_rhat). */
+typedef struct cmc_diag_view {
+  double* rhat;
+  double* mean;
+  double* sd;
+  double* ci_lo;
+  double* ci_hi;
+  int* flags;
+  double* ess;
+  int* ess_status;
+} cmc_diag_view;
+int cmc_engine_diagnostics(cmc_engine* engine, const cmc_diag_view* out,
+                           cmc_error* err);
+
 /* Profiling aid: warp-level timeline {kernel<<56|slot<<48|smid<<32|block,
  * t_start_ns, t_end_ns} of the next `sweeps` sweeps (direct launches). */
 int cmc_engine_trace(cmc_engine* engine, long m_begin, long sweeps,

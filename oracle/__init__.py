@@ -120,6 +120,8 @@ def load_ref():
     lib.ref_bench.argtypes = [c_void_p, c_int, c_long, c_long]
     lib.ref_bench.restype = c_double
     lib.ref_hardware_threads.restype = c_int
+    I = POINTER(c_int)
+    lib.ref_diagnostics.argtypes = [c_void_p, D, I, D, D, D, D, D, I, E]
     lib.ref_philox.argtypes = [U, U, U]
     lib.ref_normal_quantile.argtypes = [c_double]
     lib.ref_normal_quantile.restype = c_double
@@ -288,6 +290,22 @@ class RefEngine(_Base):
         err = CmcError()
         _check(self.lib.ref_run(self.h, views, byref(err)), err)
         return [o for o, _ in outs]
+
+    def diagnostics(self, n_cols):
+        """Reference rows (rhat, flags, mean, sd, lo, hi) and per-column ESS."""
+        G, L = self.G, self.L
+        R = 2 + 2 * L + G * (L + 1)
+        out = {k: np.zeros(R) for k in ("rhat", "mean", "sd", "lo", "hi")}
+        out["flags"] = np.zeros(R, np.int32)
+        out["ess"] = np.zeros(max(1, n_cols))
+        out["ess_status"] = np.zeros(max(1, n_cols), np.int32)
+        I = lambda a: a.ctypes.data_as(POINTER(c_int))
+        err = CmcError()
+        _check(self.lib.ref_diagnostics(self.h, dptr(out["rhat"]), I(out["flags"]),
+                                        dptr(out["mean"]), dptr(out["sd"]), dptr(out["lo"]),
+                                        dptr(out["hi"]), dptr(out["ess"]), I(out["ess_status"]),
+                                        byref(err)), err)
+        return out
 
     def bench(self, workers, burn, sweeps):
         return self.lib.ref_bench(self.h, workers, burn, sweeps)

@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "countmc/diagnostics.hpp"
 #include "countmc/engine.hpp"
 #include "countmc/errors.hpp"
 #include "countmc/model.hpp"
@@ -345,6 +346,63 @@ double ref_bench(void* h, int workers, long burn, long sweeps) {
   }
   const auto t1 = std::chrono::steady_clock::now();
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// build_diagnostics (P:src/io.cpp:507-569) numerics with the reference's
+// own gelman_rhat / credible_interval / effective_sample_size
+// (P:src/diagnostics.cpp), after GibbsEngine::run().  Row order
+// [nu|tau|theta|sigma|beta g-major|gamma]; ESS per retained column.
+int ref_diagnostics(void* h, double* rhat, int* flags, double* mean, double* sd,
+                    double* lo, double* hi, double* ess, int* ess_status, cmc_error* err) {
+  auto* r = static_cast<RefEngine*>(h);
+  std::vector<ChainOutput> outs;
+  try {
+    outs = r->engine->run();
+  } catch (const SamplerStallError& e) {
+    fill_stall(err, e);
+    return CMC_ERR_STALL;
+  }
+  const long G = r->G, L = r->L;
+  long row = 0;
+  auto one = [&](auto&& get) {
+    std::vector<MomentAccumulator> accs;
+    for (const auto& ch : outs) accs.push_back(get(ch));
+    const RhatResult rr = gelman_rhat(accs);
+    rhat[row] = rr.value;
+    double pm = 0.0, pms = 0.0;
+    for (const auto& a : accs) {
+      pm += a.mean();
+      pms += a.meansq();
+    }
+    pm /= static_cast<double>(accs.size());
+    pms /= static_cast<double>(accs.size());
+    const double var = std::max(0.0, pms - pm * pm);
+    const Interval ci = credible_interval(pm, pms, 0.05);
+    mean[row] = pm;
+    sd[row] = std::sqrt(var);
+    lo[row] = ci.lo;
+    hi[row] = ci.hi;
+    flags[row] = (rr.degenerate ? 1 : 0) | ((rr.degenerate || rr.value < 1.1) ? 2 : 0);
+    ++row;
+  };
+  one([](const ChainOutput& c) { return c.nu_acc; });
+  one([](const ChainOutput& c) { return c.tau_acc; });
+  for (long l = 0; l < L; ++l) one([l](const ChainOutput& c) { return c.theta_acc[l]; });
+  for (long l = 0; l < L; ++l) one([l](const ChainOutput& c) { return c.sigma_acc[l]; });
+  for (long g = 0; g < G; ++g)
+    for (long l = 0; l < L; ++l)
+      one([g, l, L](const ChainOutput& c) { return c.beta_acc[g * L + l]; });
+  for (long g = 0; g < G; ++g) one([g](const ChainOutput& c) { return c.gamma_acc[g]; });
+  const std::size_t ncol = outs[0].samples.size();
+  for (std::size_t col = 0; col < ncol; ++col) {
+    std::vector<std::vector<double>> series;
+    for (const auto& ch : outs) series.push_back(ch.samples[col]);
+    const EssResult e = effective_sample_size(series);
+    ess[col] = e.value;
+    ess_status[col] = e.status == EssResult::Status::ok ? 0
+                      : e.status == EssResult::Status::undefined ? 1 : 2;
+  }
+  return CMC_OK;
 }
 
 int ref_hardware_threads() {

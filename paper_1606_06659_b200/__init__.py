@@ -5,7 +5,7 @@ The compute path is ``lib/libcountmc_b200.so`` (CUDA, sm_100a) reached through
 the C-ABI in ``include/countmc_b200.h``; this package mirrors the reference's
 ``GibbsEngine`` interface on top of it.
 """
-from .engine import (ChainOutput, ChainState, ConfigError, ContrastSpec,
+from .engine import (ChainOutput, ChainState, ConfigError, ContrastSpec, Diagnostics,
                      ContrastTerm, CountMatrix, DeviceError, GibbsEngine,
                      ModelSpec, Moments, ParamRef, PriorConfig, RunConfig,
                      SamplerStallError, SimSpec, SliceConfig, TuningState,
@@ -14,7 +14,7 @@ from .engine import (ChainOutput, ChainState, ConfigError, ContrastSpec,
 from ._abi import load_library, sizes
 
 __all__ = [
-    "ChainOutput", "ChainState", "ConfigError", "ContrastSpec", "ContrastTerm",
+    "ChainOutput", "ChainState", "ConfigError", "ContrastSpec", "ContrastTerm", "Diagnostics",
     "CountMatrix", "DeviceError", "GibbsEngine", "ModelSpec", "Moments",
     "ParamRef", "PriorConfig", "RunConfig", "SamplerStallError", "SimSpec",
     "SliceConfig", "TuningState", "builtin_design", "disjunction_combine",

@@ -35,7 +35,7 @@ EXPORTS = [
     "cmc_engine_set_state", "cmc_engine_get_state", "cmc_engine_iterate",
     "cmc_engine_run", "cmc_engine_begin", "cmc_engine_sweeps", "cmc_engine_sync",
     "cmc_engine_stream", "cmc_engine_launches_per_sweep", "cmc_engine_profile",
-    "cmc_engine_trace",
+    "cmc_engine_trace", "cmc_engine_diagnostics",
     "cmc_engine_get_output",
     "cmc_simulate", "cmc_engine_shard", "cmc_nccl_unique_id", "cmc_shard_bounds",
 ]
@@ -67,6 +67,13 @@ class CmcContrastSet(ctypes.Structure):
                 ("n_coefs", POINTER(c_int)), ("threshold", POINTER(c_double)),
                 ("family", POINTER(c_int)), ("index", POINTER(c_int)),
                 ("coef", POINTER(c_double))]
+
+
+class CmcDiagView(ctypes.Structure):
+    _fields_ = [("rhat", POINTER(c_double)), ("mean", POINTER(c_double)),
+                ("sd", POINTER(c_double)), ("ci_lo", POINTER(c_double)),
+                ("ci_hi", POINTER(c_double)), ("flags", POINTER(c_int)),
+                ("ess", POINTER(c_double)), ("ess_status", POINTER(c_int))]
 
 
 class CmcOutputView(ctypes.Structure):
@@ -196,6 +203,7 @@ def load_library(path: str = LIB_PATH):
                                        POINTER(c_double), E]
     lib.cmc_engine_trace.argtypes = [c_void_p, c_long, c_long, POINTER(ctypes.c_uint64), c_long,
                                      POINTER(c_long), E]
+    lib.cmc_engine_diagnostics.argtypes = [c_void_p, POINTER(CmcDiagView), E]
     lib.cmc_engine_get_output.argtypes = [c_void_p, c_long, POINTER(CmcOutputView), E]
     lib.cmc_simulate.argtypes = [c_long, c_long, c_long, POINTER(c_double),
                                  POINTER(c_double), c_double, c_double,

@@ -1274,6 +1274,78 @@ int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
   return check_stall(e, 0, e->C, err);
 }
 
+int cmc_engine_diagnostics(cmc_engine* e, const cmc_diag_view* o, cmc_error* err) {
+  if (!e || !o || !e->begun) {
+    set_err(err, CMC_ERR_ARG, "diagnostics need a finished run()");
+    return CMC_ERR_ARG;
+  }
+  if (e->C < 2) return fail_config(err, "gelman_rhat needs at least 2 chains");
+  if (e->C > 32) return fail_config(err, "diagnostics support at most 32 chains");
+  if (e->split_tail) {
+    set_err(err, CMC_ERR_ARG, "diagnostics of a sharded engine: gather the shards first");
+    return CMC_ERR_ARG;
+  }
+  const long count =
+      std::max<long>(0, std::min(e->host_m - 1, e->cfg.burnin + e->cfg.iterations) - e->cfg.burnin);
+  if (count < 2) return fail_config(err, "gelman_rhat needs at least 2 iterations");
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  const long L = e->L, G = e->G;
+  const long R = 2 + 2 * L + G * (L + 1);
+  const long rows = std::min<long>(e->n_rows, count / e->cfg.thin);
+  DiagParams d{};
+  d.C = e->C;
+  d.L = (int)L;
+  d.N = (int)e->N;
+  d.G = G;
+  d.M = count;
+  d.n_cols = e->n_cols;
+  d.n_rows = rows;
+  d.hyper = e->hyper.p;
+  d.acc_beta = e->acc_beta.p;
+  d.acc_gam = e->acc_gam.p;
+  d.samples = e->samples.p;
+  d.z = normal_quantile(1.0 - 0.05 / 2.0);
+  // samples are stored [C][n_cols][n_rows_alloc]; the ESS kernel reads a
+  // compact [C][n_cols][rows] copy
+  DevBuf<double> out, smp;
+  DevBuf<int> fl;
+  CUDA_TRY(out.alloc((size_t)5 * R + e->n_cols));
+  CUDA_TRY(fl.alloc((size_t)R + e->n_cols));
+  CUDA_TRY(smp.alloc(std::max<size_t>(1, (size_t)e->C * e->n_cols * rows)));
+  if (rows > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(smp.p, sizeof(double) * rows, e->samples.p,
+                               sizeof(double) * e->n_rows, sizeof(double) * rows,
+                               (size_t)e->C * e->n_cols, cudaMemcpyDeviceToDevice, e->stream));
+  d.samples = smp.p;
+  d.rhat = out.p;
+  d.mean = out.p + R;
+  d.sd = out.p + 2 * R;
+  d.lo = out.p + 3 * R;
+  d.hi = out.p + 4 * R;
+  d.ess = out.p + 5 * R;
+  d.flags = fl.p;
+  d.ess_status = fl.p + R;
+  CUDA_TRY(launch_diagnostics(d, e->stream));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  double* dsts[5] = {o->rhat, o->mean, o->sd, o->ci_lo, o->ci_hi};
+  for (int k = 0; k < 5; ++k)
+    if (dsts[k])
+      CUDA_TRY(cudaMemcpy(dsts[k], out.p + (size_t)k * R, sizeof(double) * R,
+                          cudaMemcpyDeviceToHost));
+  if (o->flags) CUDA_TRY(cudaMemcpy(o->flags, fl.p, sizeof(int) * R, cudaMemcpyDeviceToHost));
+  if (o->ess && e->n_cols)
+    CUDA_TRY(cudaMemcpy(o->ess, out.p + 5 * R, sizeof(double) * e->n_cols,
+                        cudaMemcpyDeviceToHost));
+  if (o->ess_status && e->n_cols)
+    CUDA_TRY(cudaMemcpy(o->ess_status, fl.p + R, sizeof(int) * e->n_cols,
+                        cudaMemcpyDeviceToHost));
+  out.free_();
+  fl.free_();
+  smp.free_();
+  return CMC_OK;
+}
+
 // Debug timeline: record warp start/end times of the next `sweeps` sweeps
 // (direct launches on the lanes, no graph); returns the record count.
 int cmc_engine_trace(cmc_engine* e, long m_begin, long sweeps, unsigned long long* out,

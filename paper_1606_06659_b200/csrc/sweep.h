@@ -150,3 +150,27 @@ cudaError_t launch_compute_A(const double* y, const double* X, double* A,
 int gene_sweep_smem_bytes(int N, int Jmax);
 
 }  // namespace cmc
+
+namespace cmc {
+
+// Post-run diagnostics (reference build_diagnostics, P:src/io.cpp:507-569,
+// over P:src/diagnostics.cpp): rows [nu | tau | theta L | sigma L |
+// beta G x L | gamma G] (ChainOutput order), one thread per row.
+struct DiagParams {
+  int C, L, N;
+  long G, M;            // genes, monitored iterations per chain
+  long n_cols, n_rows;  // thinned samples per chain: [n_cols][n_rows]
+  const Hyper* hyper;   // [C]
+  const double* acc_beta;  // [C][4][L][G]
+  const double* acc_gam;   // [C][4][G]
+  const double* samples;   // [C][n_cols][n_rows]
+  double z;             // normal_quantile(0.975) (host libm, as the reference)
+  double *rhat, *mean, *sd, *lo, *hi;  // [R]
+  int* flags;           // [R] bit0 degenerate, bit1 pass, bit2 corrupt
+  double* ess;          // [n_cols]
+  int* ess_status;      // [n_cols] 0 ok, 1 undefined, 2 degenerate
+};
+
+cudaError_t launch_diagnostics(const DiagParams& d, cudaStream_t s);
+
+}  // namespace cmc

@@ -1098,3 +1098,164 @@ cudaError_t launch_compute_A(const double* y, const double* X, double* A,
 }
 
 }  // namespace cmc
+
+// ------------------------------------------------------ post-run diagnostics
+namespace cmc {
+namespace {
+
+// gelman_rhat (P:src/diagnostics.cpp:11-37) and the pooled estimate with
+// its credible interval (pool_moments / credible_interval, P:src/io.cpp:
+// 483-505, P:src/diagnostics.cpp:46-57) for one parameter row.
+__device__ void diag_row(const DiagParams& d, long r, const double* means,
+                         const double* meansqs) {
+  const int C = d.C;
+  const double Md = (double)d.M;
+  double grand = 0.0;
+  for (int c = 0; c < C; ++c) grand += means[c];
+  grand /= (double)C;
+  double B = 0.0, W = 0.0;
+  for (int c = 0; c < C; ++c) {
+    const double dm = means[c] - grand;
+    B += dm * dm;
+    const double v = meansqs[c] - means[c] * means[c];
+    const double var = (0.0 < v) ? v : 0.0;  // std::max(0.0, v)
+    W += (Md / (Md - 1.0)) * var;
+  }
+  B *= Md / (double)(C - 1);
+  W /= (double)C;
+  int flags = 0;
+  double rh = 1.0;
+  if (!(W > 0.0)) {
+    flags |= 1;
+  } else {
+    rh = sqrt(1.0 + (B / W - 1.0) / Md);
+  }
+  if ((flags & 1) || rh < 1.1) flags |= 2;
+  double pm = 0.0, pms = 0.0;
+  for (int c = 0; c < C; ++c) {
+    pm += means[c];
+    pms += meansqs[c];
+  }
+  pm /= (double)C;
+  pms /= (double)C;
+  const double v = pms - pm * pm;
+  const double sd = sqrt((0.0 < v) ? v : 0.0);
+  const double slack = 1e-9 * ((1.0 < fabs(pms)) ? fabs(pms) : 1.0);
+  double var = v;
+  if (var < -slack) flags |= 4;
+  if (var < 0.0) var = 0.0;
+  const double half = d.z * sqrt(var);
+  d.rhat[r] = rh;
+  d.mean[r] = pm;
+  d.sd[r] = sd;
+  d.lo[r] = pm - half;
+  d.hi[r] = pm + half;
+  d.flags[r] = flags;
+}
+
+__global__ void diag_rows_kernel(const DiagParams d) {
+  const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int L = d.L;
+  const long R = 2 + 2 * L + d.G * (L + 1);
+  if (r >= R) return;
+  double means[32], meansqs[32];
+  const int C = d.C;
+  const size_t G = (size_t)d.G;
+  for (int c = 0; c < C; ++c) {
+    if (r < 2 + 2 * L) {
+      means[c] = d.hyper[c].acc[0][r];
+      meansqs[c] = d.hyper[c].acc[1][r];
+    } else if (r < 2 + 2 * L + d.G * L) {
+      const long k = r - 2 - 2 * L, g = k / L, l = k % L;
+      const double* a = d.acc_beta + (size_t)c * 4 * L * G + (size_t)l * G + g;
+      means[c] = a[0];
+      meansqs[c] = a[(size_t)L * G];
+    } else {
+      const long g = r - 2 - 2 * L - d.G * L;
+      const double* a = d.acc_gam + (size_t)c * 4 * G + g;
+      means[c] = a[0];
+      meansqs[c] = a[G];
+    }
+  }
+  diag_row(d, r, means, meansqs);
+}
+
+// effective_sample_size for one retained column (P:src/diagnostics.cpp:
+// 80-114): one warp; each lane computes whole lag autocovariances in the
+// reference's serial order, lane 0 runs the Geyer initial-positive,
+// monotone pair scan.
+__global__ void diag_ess_kernel(const DiagParams d) {
+  extern __shared__ double lagc[];  // [n_rows] autocovariances
+  const long col = blockIdx.x;
+  const int lane = threadIdx.x;
+  const long M = d.n_rows;
+  const int C = d.C;
+  if (M < 4) {
+    if (lane == 0) {
+      d.ess[col] = 0.0;
+      d.ess_status[col] = 1;
+    }
+    return;
+  }
+  auto x = [&](int c, long i) {
+    return d.samples[((size_t)c * d.n_cols + col) * M + i];
+  };
+  __shared__ double mu[32];
+  if (lane < C) {
+    double s = 0.0;
+    for (long i = 0; i < M; ++i) s += x(lane, i);
+    mu[lane] = s / (double)M;
+  }
+  __syncwarp();
+  for (long t = lane; t < M; t += 32) {
+    double total = 0.0;
+    for (int c = 0; c < C; ++c) {
+      double s = 0.0;
+      for (long i = 0; i + t < M; ++i) s += (x(c, i) - mu[c]) * (x(c, i + t) - mu[c]);
+      total += s / (double)M;
+    }
+    lagc[t] = total / (double)C;
+  }
+  __syncwarp();
+  if (lane != 0) return;
+  const double c0 = lagc[0];
+  if (!(c0 > 0.0)) {
+    d.ess[col] = 0.0;
+    d.ess_status[col] = 2;
+    return;
+  }
+  const double total = (double)C * (double)M;
+  double tau = 0.0, prev = INFINITY;
+  for (long k = 0; 2 * k + 1 < M; ++k) {
+    const double re = lagc[2 * k] / c0;
+    const double ro = lagc[2 * k + 1] / c0;
+    double pair = re + ro;
+    if (pair <= 0.0) break;
+    pair = (prev < pair) ? prev : pair;  // std::min(pair, prev)
+    prev = pair;
+    tau += pair;
+  }
+  tau = 2.0 * tau - 1.0;
+  if (tau < 1.0) tau = 1.0;
+  d.ess[col] = total / tau;
+  d.ess_status[col] = 0;
+}
+
+}  // namespace
+
+cudaError_t launch_diagnostics(const DiagParams& d, cudaStream_t s) {
+  const long R = 2 + 2 * d.L + d.G * (d.L + 1);
+  diag_rows_kernel<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(d);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || d.n_cols == 0) return e;
+  const size_t smem = sizeof(double) * (size_t)(d.n_rows > 0 ? d.n_rows : 1);
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(diag_ess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  diag_ess_kernel<<<(unsigned)d.n_cols, 32, smem, s>>>(d);
+  return cudaGetLastError();
+}
+
+}  // namespace cmc

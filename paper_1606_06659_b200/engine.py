@@ -240,6 +240,22 @@ class ContrastResult:
 
 
 @dataclass
+class Diagnostics:
+    """Per-parameter convergence diagnostics (reference DiagRow,
+    P:include/countmc/io.hpp, build_diagnostics P:src/io.cpp:507-569)."""
+    names: List[str]
+    rhat: np.ndarray
+    degenerate: np.ndarray
+    passed: np.ndarray
+    mean: np.ndarray
+    sd: np.ndarray
+    ci_lo: np.ndarray
+    ci_hi: np.ndarray
+    ess: np.ndarray          # NaN where the parameter is not retained
+    ess_status: List[str]    # ok / undefined / degenerate / not-retained
+
+
+@dataclass
 class ChainOutput:
     chain: int
     nu_acc: Moments
@@ -469,6 +485,42 @@ class GibbsEngine:
             _raise(self._lib.cmc_engine_sync(self._h, byref(err)), err)
             self._outputs = [self._output(c) for c in range(self._cfg.chains)]
         return self._outputs
+
+    def diagnostics(self) -> Diagnostics:
+        """R-hat, pooled estimates and ESS for every parameter, computed on
+        the device from the resident accumulators of the last run()."""
+        self.run()
+        G, L = self.G, self.L
+        R = 2 + 2 * L + G * (L + 1)
+        arr = {k: np.zeros(R) for k in ("rhat", "mean", "sd", "lo", "hi")}
+        flags = np.zeros(R, dtype=np.int32)
+        ess = np.zeros(max(1, self.n_cols))
+        est = np.zeros(max(1, self.n_cols), dtype=np.int32)
+        view = _abi.CmcDiagView(dptr(arr["rhat"]), dptr(arr["mean"]), dptr(arr["sd"]),
+                                dptr(arr["lo"]), dptr(arr["hi"]),
+                                flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), dptr(ess),
+                                est.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+        err = CmcError()
+        _raise(self._lib.cmc_engine_diagnostics(self._h, byref(view), byref(err)), err)
+        names = ["nu", "tau"] + [f"theta[{l + 1}]" for l in range(L)] + \
+                [f"sigma[{l + 1}]" for l in range(L)]
+        names += [f"beta[{g + 1},{l + 1}]" for g in range(G) for l in range(L)]
+        names += [f"gamma[{g + 1}]" for g in range(G)]
+        row_ess = np.full(R, np.nan)
+        status = ["not-retained"] * R
+        code = {0: "ok", 1: "undefined", 2: "degenerate"}
+        col_of = {}
+        for c in range(2 + 2 * L):
+            col_of[c] = c
+        for k, g in enumerate(self._saved):
+            for l in range(L):
+                col_of[2 + 2 * L + g * L + l] = 2 + 2 * L + k * (L + 1) + l
+            col_of[2 + 2 * L + G * L + g] = 2 + 2 * L + k * (L + 1) + L
+        for r, c in col_of.items():
+            row_ess[r] = ess[c] if est[c] == 0 else (np.nan if est[c] == 1 else ess[c])
+            status[r] = code[int(est[c])]
+        return Diagnostics(names, arr["rhat"], (flags & 1) != 0, (flags & 2) != 0, arr["mean"],
+                           arr["sd"], arr["lo"], arr["hi"], row_ess, status)
 
     def run_chain(self, chain: int) -> ChainOutput:
         return self.run()[chain]
