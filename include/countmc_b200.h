@@ -38,6 +38,7 @@ extern "C" {
 #define CMC_ERR_CUDA 3   /* device/runtime failure                         */
 #define CMC_ERR_NCCL 4   /* collective failure (multi-GPU)                 */
 #define CMC_ERR_ARG 5    /* bad pointer / index at the boundary            */
+#define CMC_ERR_LOAD 6   /* reference LoadError (errors.hpp:16-19)         */
 
 /* Sampler modes, reference SamplerMode (engine.hpp:19). */
 #define CMC_SLICE_FAITHFUL 0
@@ -261,6 +262,34 @@ int cmc_engine_shard(cmc_engine* engine, int rank, int world,
 int cmc_nccl_unique_id(void* out128, cmc_error* err);
 /* Shard bounds for gene count G over `world` ranks (leaf aligned). */
 int cmc_shard_bounds(long G, int rank, int world, long* g_begin, long* g_end);
+
+/* ---- Input side, host, multithreaded ---- */
+
+/* Parsed counts CSV; replaces countmc::CountMatrix from load_counts
+ * (P:src/io.cpp:125-164).  Header "gene,<sample>..." (>= 2 cells, quoted
+ * cells per split_csv io.cpp:46-76), one row per gene with N+1 cells, empty
+ * rows skipped, CRLF accepted.  Errors are CMC_ERR_LOAD with the
+ * reference's LoadError message for the first bad row in file order. */
+typedef struct cmc_counts cmc_counts;
+int cmc_counts_load(const char* path, cmc_counts** out, cmc_error* err);
+int cmc_counts_dims(const cmc_counts* counts, long* G, long* N,
+                    int* duplicate_genes);
+/* G x N row-major, valid until cmc_counts_free. */
+const long long* cmc_counts_data(const cmc_counts* counts);
+const char* cmc_counts_gene(const cmc_counts* counts, long g);
+const char* cmc_counts_sample(const cmc_counts* counts, long n);
+/* All labels at once: which = 0 genes, 1 samples; *blob holds them
+ * NUL-terminated back to back (*bytes in total, in row/column order). */
+int cmc_counts_labels(const cmc_counts* counts, int which, const char** blob,
+                      size_t* bytes);
+void cmc_counts_free(cmc_counts* counts);
+
+/* Median-of-ratios offsets, replaces countmc::estimate_offsets
+ * (P:src/model.cpp:21-68; bit-identical).  counts is G x N row-major;
+ * h_out has N entries.  No gene positive in every sample -> CMC_ERR_CONFIG
+ * with the reference's NormalizationError message. */
+int cmc_estimate_offsets(long G, long N, const long long* counts,
+                         double* h_out, cmc_error* err);
 
 #ifdef __cplusplus
 }

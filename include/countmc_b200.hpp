@@ -45,12 +45,59 @@ class DeviceError : public std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+class LoadError : public std::runtime_error {  // P:include/countmc/errors.hpp:16
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+class NormalizationError : public ConfigError {  // P:include/countmc/errors.hpp:22
+ public:
+  using ConfigError::ConfigError;
+};
+
 inline void check(int rc, const cmc_error& e) {
   if (rc == CMC_OK) return;
   if (rc == CMC_ERR_CONFIG) throw ConfigError(e.msg);
   if (rc == CMC_ERR_STALL) throw SamplerStallError(e);
   if (rc == CMC_ERR_ARG) throw std::invalid_argument(e.msg);
+  if (rc == CMC_ERR_LOAD) throw LoadError(e.msg);
   throw DeviceError(e.msg);
+}
+
+// CountMatrix (P:include/countmc/types.hpp:50-58): G x N row-major counts.
+struct CountMatrix {
+  long G = 0, N = 0;
+  std::vector<long long> counts;
+  std::vector<std::string> genes, samples;
+  bool duplicate_genes = false;
+};
+
+// load_counts (P:src/io.cpp:125-164), multithreaded; throws LoadError.
+inline CountMatrix load_counts(const std::string& path) {
+  cmc_counts* h = nullptr;
+  cmc_error e{};
+  check(cmc_counts_load(path.c_str(), &h, &e), e);
+  CountMatrix m;
+  int dup = 0;
+  cmc_counts_dims(h, &m.G, &m.N, &dup);
+  m.duplicate_genes = dup != 0;
+  const long long* d = cmc_counts_data(h);
+  m.counts.assign(d, d + m.G * m.N);
+  for (long g = 0; g < m.G; ++g) m.genes.emplace_back(cmc_counts_gene(h, g));
+  for (long n = 0; n < m.N; ++n) m.samples.emplace_back(cmc_counts_sample(h, n));
+  cmc_counts_free(h);
+  return m;
+}
+
+// estimate_offsets (P:src/model.cpp:21-68), bit-identical; throws
+// NormalizationError when no gene is positive in every sample.
+inline std::vector<double> estimate_offsets(const CountMatrix& m) {
+  std::vector<double> h(static_cast<size_t>(m.N));
+  cmc_error e{};
+  const int rc = cmc_estimate_offsets(m.G, m.N, m.counts.data(), h.data(), &e);
+  if (rc == CMC_ERR_CONFIG) throw NormalizationError(e.msg);
+  check(rc, e);
+  return h;
 }
 
 enum class SamplerMode { slice_faithful, conjugate_direct };

@@ -135,6 +135,11 @@ def load_ref():
     lib.ref_log_fc_sigma.restype = c_double
     lib.ref_pairwise_sum.argtypes = [D, c_long]
     lib.ref_pairwise_sum.restype = c_double
+    lib.ref_load_counts.argtypes = [ctypes.c_char_p, POINTER(c_longlong), c_long,
+                                    ctypes.c_char_p, c_long, POINTER(c_long), POINTER(c_long),
+                                    I, ctypes.c_char_p]
+    lib.ref_estimate_offsets.argtypes = [c_long, c_long, POINTER(c_longlong), D,
+                                         ctypes.c_char_p]
     _REF = lib
     return lib
 
@@ -319,3 +324,50 @@ def heterosis16x5(N=16):
         X[n, :4] = A[(n % 16) // 4]
         X[n, 4] = block[n % 4]
     return X
+
+
+def ref_load_counts(path):
+    """The reference's own load_counts (P:src/io.cpp:125-164).  Returns
+    (counts, genes, samples, duplicate_genes) or raises RefLoadError /
+    ConfigErr with the reference's message."""
+    lib = load_ref()
+    cap_cells, cap_names = 1 << 16, 1 << 20
+    while True:
+        cells = np.zeros(cap_cells, np.int64)
+        names = ctypes.create_string_buffer(cap_names)
+        G, N, dup = c_long(), c_long(), ctypes.c_int()
+        msg = ctypes.create_string_buffer(256)
+        rc = lib.ref_load_counts(str(path).encode(),
+                                 cells.ctypes.data_as(POINTER(c_longlong)), cap_cells,
+                                 names, cap_names, ctypes.byref(G), ctypes.byref(N),
+                                 ctypes.byref(dup), msg)
+        if rc == -1:
+            cap_cells = max(cap_cells, G.value * N.value)
+            cap_names *= 4
+            continue
+        if rc == 6:
+            raise RefLoadError(msg.value.decode(errors="replace"))
+        if rc == 1:
+            raise ConfigErr(msg.value.decode(errors="replace"))
+        G, N = G.value, N.value
+        parts = names.raw.split(b"\0")[:N + G]
+        samples = [p.decode(errors="surrogateescape") for p in parts[:N]]
+        genes = [p.decode(errors="surrogateescape") for p in parts[N:]]
+        return cells[:G * N].reshape(G, N).copy(), genes, samples, bool(dup.value)
+
+
+def ref_estimate_offsets(counts):
+    """The reference's estimate_offsets (P:src/model.cpp:21-68)."""
+    lib = load_ref()
+    y = np.ascontiguousarray(counts, dtype=np.int64)
+    h = np.zeros(y.shape[1])
+    msg = ctypes.create_string_buffer(256)
+    rc = lib.ref_estimate_offsets(y.shape[0], y.shape[1], y.ctypes.data_as(POINTER(c_longlong)),
+                                  h.ctypes.data_as(POINTER(c_double)), msg)
+    if rc:
+        raise ConfigErr(msg.value.decode(errors="replace"))
+    return h
+
+
+class RefLoadError(RuntimeError):
+    """LoadError raised by the reference loader."""

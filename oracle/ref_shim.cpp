@@ -17,6 +17,7 @@
 #include "countmc/diagnostics.hpp"
 #include "countmc/engine.hpp"
 #include "countmc/errors.hpp"
+#include "countmc/io.hpp"
 #include "countmc/model.hpp"
 #include "countmc/parallel.hpp"
 #include "countmc/rng.hpp"
@@ -403,6 +404,49 @@ int ref_diagnostics(void* h, double* rhat, int* flags, double* mean, double* sd,
                       : e.status == EssResult::Status::undefined ? 1 : 2;
   }
   return CMC_OK;
+}
+
+// ---- input side: load_counts (P:src/io.cpp:125-164), estimate_offsets
+// (P:src/model.cpp:21-68).  Returns 0, 6 (LoadError), 1 (ConfigError) or
+// -1 when cells/names capacity is short (G, N still written).  Names are
+// NUL-separated: samples first, then genes.
+int ref_load_counts(const char* path, long long* cells, long cap_cells, char* names,
+                    long cap_names, long* G, long* N, int* dup, char* msg) {
+  try {
+    const CountMatrix m = load_counts(path);
+    *G = static_cast<long>(m.G());
+    *N = static_cast<long>(m.N());
+    *dup = m.duplicate_genes ? 1 : 0;
+    std::string all;
+    for (const auto& s : m.samples) all.append(s).push_back('\0');
+    for (const auto& g : m.genes) all.append(g).push_back('\0');
+    if (cap_cells < *G * *N || cap_names < static_cast<long>(all.size())) return -1;
+    std::memcpy(cells, m.counts.data().data(), sizeof(long long) * m.counts.data().size());
+    std::memcpy(names, all.data(), all.size());
+    return 0;
+  } catch (const LoadError& e) {
+    std::snprintf(msg, 256, "%s", e.what());
+    return 6;
+  } catch (const ConfigError& e) {
+    std::snprintf(msg, 256, "%s", e.what());
+    return 1;
+  }
+}
+
+int ref_estimate_offsets(long G, long N, const long long* counts, double* h, char* msg) {
+  CountMatrix m;
+  m.counts = Grid<long long>(G, N, 0);
+  std::memcpy(m.counts.data().data(), counts, sizeof(long long) * G * N);
+  for (long g = 0; g < G; ++g) m.genes.push_back("g" + std::to_string(g));
+  for (long n = 0; n < N; ++n) m.samples.push_back("s" + std::to_string(n));
+  try {
+    const std::vector<double> out = estimate_offsets(m);
+    std::memcpy(h, out.data(), sizeof(double) * N);
+    return 0;
+  } catch (const ConfigError& e) {
+    std::snprintf(msg, 256, "%s", e.what());
+    return 1;
+  }
 }
 
 int ref_hardware_threads() {

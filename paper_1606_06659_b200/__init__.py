@@ -7,7 +7,8 @@ the C-ABI in ``include/countmc_b200.h``; this package mirrors the reference's
 """
 from .engine import (ChainOutput, ChainState, ConfigError, ContrastSpec, Diagnostics,
                      ContrastTerm, CountMatrix, DeviceError, GibbsEngine,
-                     ModelSpec, Moments, ParamRef, PriorConfig, RunConfig,
+                     LoadError, ModelSpec, Moments, NormalizationError, ParamRef,
+                     PriorConfig, RunConfig, estimate_offsets, load_counts,
                      SamplerStallError, SimSpec, SliceConfig, TuningState,
                      builtin_design, disjunction_combine, generate,
                      heterosis_contrast, parse_param_ref)
@@ -15,7 +16,8 @@ from ._abi import load_library, sizes
 
 __all__ = [
     "ChainOutput", "ChainState", "ConfigError", "ContrastSpec", "ContrastTerm", "Diagnostics",
-    "CountMatrix", "DeviceError", "GibbsEngine", "ModelSpec", "Moments",
+    "CountMatrix", "DeviceError", "GibbsEngine", "LoadError", "ModelSpec", "Moments",
+    "NormalizationError", "estimate_offsets", "load_counts",
     "ParamRef", "PriorConfig", "RunConfig", "SamplerStallError", "SimSpec",
     "SliceConfig", "TuningState", "builtin_design", "disjunction_combine",
     "generate", "heterosis_contrast", "parse_param_ref", "load_library", "sizes",

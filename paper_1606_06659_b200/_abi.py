@@ -22,6 +22,7 @@ CMC_ERR_STALL = 2
 CMC_ERR_CUDA = 3
 CMC_ERR_NCCL = 4
 CMC_ERR_ARG = 5
+CMC_ERR_LOAD = 6
 
 CMC_SLICE_FAITHFUL = 0
 CMC_CONJUGATE_DIRECT = 1
@@ -38,6 +39,8 @@ EXPORTS = [
     "cmc_engine_trace", "cmc_engine_diagnostics",
     "cmc_engine_get_output",
     "cmc_simulate", "cmc_engine_shard", "cmc_nccl_unique_id", "cmc_shard_bounds",
+    "cmc_counts_load", "cmc_counts_dims", "cmc_counts_data", "cmc_counts_gene",
+    "cmc_counts_sample", "cmc_counts_labels", "cmc_counts_free", "cmc_estimate_offsets",
 ]
 
 
@@ -212,5 +215,19 @@ def load_library(path: str = LIB_PATH):
     lib.cmc_engine_shard.argtypes = [c_void_p, c_int, c_int, c_void_p, E]
     lib.cmc_nccl_unique_id.argtypes = [c_void_p, E]
     lib.cmc_shard_bounds.argtypes = [c_long, c_int, c_int, POINTER(c_long), POINTER(c_long)]
+    lib.cmc_counts_load.argtypes = [ctypes.c_char_p, POINTER(c_void_p), E]
+    lib.cmc_counts_dims.argtypes = [c_void_p, POINTER(c_long), POINTER(c_long), POINTER(c_int)]
+    lib.cmc_counts_data.argtypes = [c_void_p]
+    lib.cmc_counts_data.restype = POINTER(c_longlong)
+    lib.cmc_counts_gene.argtypes = [c_void_p, c_long]
+    lib.cmc_counts_gene.restype = ctypes.c_char_p
+    lib.cmc_counts_sample.argtypes = [c_void_p, c_long]
+    lib.cmc_counts_sample.restype = ctypes.c_char_p
+    lib.cmc_counts_labels.argtypes = [c_void_p, c_int, POINTER(ctypes.c_char_p),
+                                      POINTER(ctypes.c_size_t)]
+    lib.cmc_counts_free.argtypes = [c_void_p]
+    lib.cmc_counts_free.restype = None
+    lib.cmc_estimate_offsets.argtypes = [c_long, c_long, POINTER(c_longlong),
+                                         POINTER(c_double), E]
     _LIB = lib
     return lib

@@ -50,6 +50,14 @@ class DeviceError(RuntimeError):
     """CUDA / NCCL failure inside the library."""
 
 
+class LoadError(RuntimeError):
+    """Malformed input file (reference LoadError, errors.hpp:16-19)."""
+
+
+class NormalizationError(ConfigError):
+    """No gene positive in every sample (reference NormalizationError)."""
+
+
 def _raise(rc: int, err: CmcError):
     if rc == _abi.CMC_OK:
         return
@@ -61,6 +69,8 @@ def _raise(rc: int, err: CmcError):
                                 err.x0, err.width, err.iteration)
     if rc == _abi.CMC_ERR_ARG:
         raise ValueError(msg)
+    if rc == _abi.CMC_ERR_LOAD:
+        raise LoadError(msg)
     raise DeviceError(msg)
 
 
@@ -134,7 +144,11 @@ class ModelSpec:
 
 @dataclass
 class CountMatrix:
+    """Reference CountMatrix (P:include/countmc/types.hpp:50-58)."""
     counts: np.ndarray  # G x N int64
+    genes: Optional[List[str]] = None
+    samples: Optional[List[str]] = None
+    duplicate_genes: bool = False
 
     @property
     def G(self):
@@ -608,6 +622,55 @@ def generate(spec: SimSpec) -> CountMatrix:
                           out.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), byref(err))
     _raise(rc, err)
     return CountMatrix(out)
+
+
+def _labels(lib, h, which, n):
+    blob, size = ctypes.c_char_p(), ctypes.c_size_t()
+    lib.cmc_counts_labels(h, which, byref(blob), byref(size))
+    raw = ctypes.string_at(blob, size.value)
+    return raw.decode(errors="surrogateescape").split("\0")[:n]
+
+
+def load_counts(path: str) -> CountMatrix:
+    """Counts CSV -> CountMatrix, same rules and LoadError messages as the
+    reference load_counts (P:src/io.cpp:125-164); parsed by the library's
+    multithreaded host loader (cmc_counts_load)."""
+    lib = load_library()
+    h = c_void_p()
+    err = CmcError()
+    _raise(lib.cmc_counts_load(str(path).encode(), byref(h), byref(err)), err)
+    try:
+        G, N, dup = c_long(), c_long(), ctypes.c_int()
+        lib.cmc_counts_dims(h, byref(G), byref(N), byref(dup))
+        G, N = G.value, N.value
+        counts = np.ctypeslib.as_array(lib.cmc_counts_data(h), shape=(G * N,))
+        counts = counts.astype(np.int64, copy=True).reshape(G, N)
+        genes, samples = (_labels(lib, h, which, n) for which, n in ((0, G), (1, N)))
+    finally:
+        lib.cmc_counts_free(h)
+    return CountMatrix(counts, genes, samples, bool(dup.value))
+
+
+def estimate_offsets(counts) -> np.ndarray:
+    """Median-of-ratios log offsets h (reference estimate_offsets,
+    P:src/model.cpp:21-68, bit-identical); raises NormalizationError when no
+    gene is positive in every sample."""
+    lib = load_library()
+    y = counts.counts if isinstance(counts, CountMatrix) else counts
+    y = np.ascontiguousarray(y, dtype=np.int64)
+    if y.ndim != 2:
+        raise ValueError("counts must be a G x N matrix")
+    G, N = y.shape
+    if G < 1 or N < 1:
+        raise ConfigError("count matrix must have at least one gene and one sample")
+    h = np.zeros(N)
+    err = CmcError()
+    rc = lib.cmc_estimate_offsets(G, N, y.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)),
+                                  dptr(h), byref(err))
+    if rc == _abi.CMC_ERR_CONFIG:
+        raise NormalizationError(err.msg.decode(errors="replace"))
+    _raise(rc, err)
+    return h
 
 
 def builtin_design(name: str, N: int) -> np.ndarray:
