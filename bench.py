@@ -84,12 +84,14 @@ def cpu_model():
     return "unknown"
 
 
-def reference_rate(counts, X, h, burnin, warmup, steps=None, seconds=None):
-    """The reference's own iterate + monitors on all host threads
-    (oracle/_ref shim ref_bench).  Returns (gene-iter/s, threads, sweeps, s)."""
+def reference_rate(counts, X, h, burnin, warmup, steps=None, seconds=None, workers=None):
+    """The reference's own iterate + monitors on all host threads, or on
+    `workers` threads after an all-thread burn-in (oracle/_ref shim
+    ref_bench_split).  Returns (gene-iter/s, threads, sweeps, s, kind)."""
     import oracle
     from paper_1606_06659_b200 import _abi
-    threads = nproc()
+    all_threads = nproc()
+    threads = workers or all_threads
     cfg = _abi.make_config(chains=1, burnin=burnin, iterations=10 ** 6, thin=20, seed=7,
                            save_genes=20, workers=threads)
     heter = [([("beta_col", 1, 2.0), ("beta_col", 3, 1.0)], 0.0),
@@ -101,9 +103,9 @@ def reference_rate(counts, X, h, burnin, warmup, steps=None, seconds=None):
         raise RuntimeError("oracle/_ref/libcountmc_ref.so missing")
     G = counts.shape[0]
     if steps is None:
-        probe = eng.bench(threads, burnin + warmup, 3)
+        probe = eng.bench(threads, burnin + warmup, 3, burn_workers=all_threads)
         steps = max(3, int(seconds / max(probe / 3, 1e-6)))
-    secs = eng.bench(threads, burnin + warmup, steps)
+    secs = eng.bench(threads, burnin + warmup, steps, burn_workers=all_threads)
     return G * steps / secs, threads, steps, secs, kind
 
 
@@ -208,10 +210,25 @@ def run_b200(a, rank, world, local_rank):
             raise RuntimeError(err.msg.decode())
 
     ok(lib.cmc_engine_begin(hd, byref(err)))
-    ok(lib.cmc_engine_sweeps(hd, 1, B + 1, byref(err)))          # burn-in: tune widths
+    stream = torch.cuda.ExternalStream(lib.cmc_engine_stream(hd))
+    # burn-in (tuning active, no monitors), timed separately;
+    # sweeps 1..5 start from w_init = 1 (the divergent-slice-loop proxy, config 3)
+    nb0 = min(5, B)
+    b0, b1, b2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    b0.record(stream)
+    ok(lib.cmc_engine_sweeps(hd, 1, 1 + nb0, byref(err)))
+    b1.record(stream)
+    ok(lib.cmc_engine_sweeps(hd, 1 + nb0, B + 1, byref(err)))    # rest of burn-in
+    b2.record(stream)
     ok(lib.cmc_engine_sweeps(hd, B + 1, B + 1 + W, byref(err)))  # warm-up monitored steps
     ok(lib.cmc_engine_sync(hd, byref(err)))
-    stream = torch.cuda.ExternalStream(lib.cmc_engine_stream(hd))
+    burn_first_ms, burn_rest_ms = b0.elapsed_time(b1), b1.elapsed_time(b2)
+    burnin = {"value": C * G * B / ((burn_first_ms + burn_rest_ms) * 1e-3),
+              "unit": "gene-iter/s", "sweeps": B,
+              "ms_per_sweep": (burn_first_ms + burn_rest_ms) / B,
+              "first_sweeps": nb0, "first_ms_per_sweep": burn_first_ms / max(nb0, 1),
+              "note": "burn-in sweeps (tuning on, no monitors), one GPU, device-timed; "
+                      "first_* are sweeps 1..5 from w_init=1 (wide, divergent slice loops)"}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         torch.distributed.barrier()
@@ -318,6 +335,11 @@ def run_b200(a, rank, world, local_rank):
                    "sample": f"{steps} monitored sweeps of 1 chain at G={G} after {B + W} "
                              f"burn-in sweeps, reference iterate()+monitors, workers={threads}, "
                              f"{cpu_model()}"}
+            r1, _, s1, _, _ = reference_rate(counts, X, h, B, W, seconds=a.cpu_seconds / 3,
+                                             workers=1)
+            cpu["single_core"] = {"value": r1, "cores": 1,
+                                  "sample": f"{s1} monitored sweeps, workers=1 (burn-in on "
+                                            f"all threads)"}
         except Exception as ex:  # report, never fake
             cpu = {"value": None, "unit": "gene-iter/s", "cores": nproc(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -336,6 +358,7 @@ def run_b200(a, rank, world, local_rank):
                          % (C * G * bytes_per_gene_iter(16, 5, 1) / 1e6 + G * 16 * 8 / 1e6)},
         "gpu_launches": launches,
         "clocks": clk,
+        "burnin": burnin,
         "e2e": e2e,
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -263,6 +263,20 @@ int cmc_nccl_unique_id(void* out128, cmc_error* err);
 /* Shard bounds for gene count G over `world` ranks (leaf aligned). */
 int cmc_shard_bounds(long G, int rank, int world, long* g_begin, long* g_end);
 
+/* Results files, replaces countmc::write_results (P:src/io.cpp:571-720):
+ * gene_estimates.csv, hyper_estimates.csv, diagnostics.csv,
+ * samples/chain_<c>.csv and run_report.json under outdir, from the
+ * device-resident accumulators (diagnostics on the device, parallel host
+ * formatting).  genes: G labels (NULL -> "g1".."gG", the names generate()
+ * gives); contrast_ids: one id per contrast passed to create (NULL ->
+ * "contrast<k>").  The CSV bytes equal the reference's for equal inputs.
+ * Fewer than 2 chains or 2 monitored iterations: the estimate files are
+ * written, then CMC_ERR_CONFIG as build_diagnostics throws. */
+int cmc_engine_write_results(cmc_engine* engine, const char* outdir,
+                             const char* const* genes,
+                             const char* const* contrast_ids,
+                             double wall_seconds, cmc_error* err);
+
 /* ---- Input side, host, multithreaded ---- */
 
 /* Parsed counts CSV; replaces countmc::CountMatrix from load_counts

@@ -119,6 +119,10 @@ def load_ref():
     lib.ref_run.argtypes = [c_void_p, POINTER(CmcOutputView), E]
     lib.ref_bench.argtypes = [c_void_p, c_int, c_long, c_long]
     lib.ref_bench.restype = c_double
+    lib.ref_write_results.argtypes = [c_void_p, ctypes.c_char_p, POINTER(ctypes.c_char_p),
+                                      c_double, D, E]
+    lib.ref_bench_split.argtypes = [c_void_p, c_int, c_int, c_long, c_long]
+    lib.ref_bench_split.restype = c_double
     lib.ref_hardware_threads.restype = c_int
     I = POINTER(c_int)
     lib.ref_diagnostics.argtypes = [c_void_p, D, I, D, D, D, D, D, I, E]
@@ -312,8 +316,24 @@ class RefEngine(_Base):
                                         byref(err)), err)
         return out
 
-    def bench(self, workers, burn, sweeps):
-        return self.lib.ref_bench(self.h, workers, burn, sweeps)
+    def write_results(self, outdir, genes=None, wall_seconds=0.0):
+        """run() then the reference's write_results into outdir; returns the
+        seconds write_results itself took."""
+        gl = None
+        if genes is not None:
+            gl = (ctypes.c_char_p * len(genes))(*[g.encode() for g in genes])
+        secs = c_double()
+        err = CmcError()
+        rc = self.lib.ref_write_results(self.h, str(outdir).encode(), gl, wall_seconds,
+                                        ctypes.byref(secs), ctypes.byref(err))
+        if rc == _abi.CMC_ERR_CONFIG:
+            raise ConfigErr(err.msg.decode())
+        if rc:
+            raise StallError(err.msg.decode())
+        return secs.value
+
+    def bench(self, workers, burn, sweeps, burn_workers=None):
+        return self.lib.ref_bench_split(self.h, burn_workers or workers, workers, burn, sweeps)
 
 
 def heterosis16x5(N=16):

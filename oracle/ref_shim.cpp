@@ -304,11 +304,42 @@ int ref_run(void* h, const cmc_output_view* outputs, cmc_error* err) {
   return CMC_OK;
 }
 
+// The reference's own run() + write_results (P:src/io.cpp:571-720) into
+// outdir; genes (G labels) may be NULL (keeps "g<g+1>").  Returns the
+// seconds write_results took in *write_s.
+int ref_write_results(void* h, const char* outdir, const char* const* genes,
+                      double wall_seconds, double* write_s, cmc_error* err) {
+  auto* r = static_cast<RefEngine*>(h);
+  try {
+    if (genes)
+      for (long g = 0; g < r->G; ++g) r->data.genes[g] = genes[g];
+    const auto outs = r->engine->run();
+    const auto t0 = std::chrono::steady_clock::now();
+    write_results(outdir, r->data, r->spec, r->engine->config(), outs, wall_seconds);
+    *write_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  } catch (const SamplerStallError& e) {
+    fill_stall(err, e);
+    return CMC_ERR_STALL;
+  } catch (const ConfigError& e) {
+    fill_err(err, CMC_ERR_CONFIG, e.what());
+    return CMC_ERR_CONFIG;
+  }
+  return CMC_OK;
+}
+
 // CPU baseline: the reference's own iterate() plus run_chain's monitored
 // loop body (P:src/engine.cpp:409-431: moment and contrast accumulators),
 // `burn` un-timed burn-in sweeps then `sweeps` timed sweeps on `workers`
 // threads.  Returns wall seconds of the timed sweeps.
+double ref_bench_split(void* h, int burn_workers, int workers, long burn, long sweeps);
+
 double ref_bench(void* h, int workers, long burn, long sweeps) {
+  return ref_bench_split(h, workers, workers, burn, sweeps);
+}
+
+// Burn-in on burn_workers threads, then `sweeps` monitored sweeps timed on
+// `workers` threads (iterate is bitwise independent of the worker count).
+double ref_bench_split(void* h, int burn_workers, int workers, long burn, long sweeps) {
   auto* r = static_cast<RefEngine*>(h);
   const auto& cfg = r->engine->config();
   const long G = r->G, N = r->N, L = r->L;
@@ -316,14 +347,17 @@ double ref_bench(void* h, int workers, long burn, long sweeps) {
   TuningState tuning(G, N, L, cfg.slice.w_init);
   EngineScratch scratch(G, N);
   ClampCounter clamps;
-  ThreadPool pool(workers);
   std::vector<MomentAccumulator> theta_acc(L), sigma_acc(L), beta_acc(G * L),
       gamma_acc(G), eps_acc(G * N);
   MomentAccumulator nu_acc, tau_acc;
   std::vector<ContrastAccumulator> contrasts;
   for (const auto& spec : r->engine->contrast_specs()) contrasts.emplace_back(spec, G);
-  for (long m = 1; m <= burn; ++m)
-    r->engine->iterate(state, tuning, 0, m, pool, scratch, &clamps);
+  {
+    ThreadPool burn_pool(burn_workers);
+    for (long m = 1; m <= burn; ++m)
+      r->engine->iterate(state, tuning, 0, m, burn_pool, scratch, &clamps);
+  }
+  ThreadPool pool(workers);
   const auto t0 = std::chrono::steady_clock::now();
   for (long m = burn + 1; m <= burn + sweeps; ++m) {
     r->engine->iterate(state, tuning, 0, m, pool, scratch, &clamps);

@@ -36,7 +36,7 @@ EXPORTS = [
     "cmc_engine_set_state", "cmc_engine_get_state", "cmc_engine_iterate",
     "cmc_engine_run", "cmc_engine_begin", "cmc_engine_sweeps", "cmc_engine_sync",
     "cmc_engine_stream", "cmc_engine_launches_per_sweep", "cmc_engine_profile",
-    "cmc_engine_trace", "cmc_engine_diagnostics",
+    "cmc_engine_trace", "cmc_engine_diagnostics", "cmc_engine_write_results",
     "cmc_engine_get_output",
     "cmc_simulate", "cmc_engine_shard", "cmc_nccl_unique_id", "cmc_shard_bounds",
     "cmc_counts_load", "cmc_counts_dims", "cmc_counts_data", "cmc_counts_gene",
@@ -207,6 +207,9 @@ def load_library(path: str = LIB_PATH):
     lib.cmc_engine_trace.argtypes = [c_void_p, c_long, c_long, POINTER(ctypes.c_uint64), c_long,
                                      POINTER(c_long), E]
     lib.cmc_engine_diagnostics.argtypes = [c_void_p, POINTER(CmcDiagView), E]
+    lib.cmc_engine_write_results.argtypes = [c_void_p, ctypes.c_char_p,
+                                             POINTER(ctypes.c_char_p), POINTER(ctypes.c_char_p),
+                                             c_double, E]
     lib.cmc_engine_get_output.argtypes = [c_void_p, c_long, POINTER(CmcOutputView), E]
     lib.cmc_simulate.argtypes = [c_long, c_long, c_long, POINTER(c_double),
                                  POINTER(c_double), c_double, c_double,

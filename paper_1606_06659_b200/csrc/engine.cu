@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/countmc_b200.h"
+#include "output_host.h"
 #include "rng.cuh"
 #include "sweep.h"
 
@@ -1274,20 +1275,11 @@ int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
   return check_stall(e, 0, e->C, err);
 }
 
-int cmc_engine_diagnostics(cmc_engine* e, const cmc_diag_view* o, cmc_error* err) {
-  if (!e || !o || !e->begun) {
-    set_err(err, CMC_ERR_ARG, "diagnostics need a finished run()");
-    return CMC_ERR_ARG;
-  }
-  if (e->C < 2) return fail_config(err, "gelman_rhat needs at least 2 chains");
-  if (e->C > 32) return fail_config(err, "diagnostics support at most 32 chains");
-  if (e->split_tail) {
-    set_err(err, CMC_ERR_ARG, "diagnostics of a sharded engine: gather the shards first");
-    return CMC_ERR_ARG;
-  }
-  const long count =
-      std::max<long>(0, std::min(e->host_m - 1, e->cfg.burnin + e->cfg.iterations) - e->cfg.burnin);
-  if (count < 2) return fail_config(err, "gelman_rhat needs at least 2 iterations");
+// Runs the diagnostics kernels over the resident accumulators and copies
+// [rhat | mean | sd | lo | hi] (5R), ess (n_cols) and [flags R | ess_status
+// n_cols] to the host.  count = monitored iterations per chain.
+static int diag_to_host(cmc_engine* e, long count, std::vector<double>& vals,
+                        std::vector<int>& flags, cmc_error* err) {
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   const long L = e->L, G = e->G;
@@ -1304,7 +1296,6 @@ int cmc_engine_diagnostics(cmc_engine* e, const cmc_diag_view* o, cmc_error* err
   d.hyper = e->hyper.p;
   d.acc_beta = e->acc_beta.p;
   d.acc_gam = e->acc_gam.p;
-  d.samples = e->samples.p;
   d.z = normal_quantile(1.0 - 0.05 / 2.0);
   // samples are stored [C][n_cols][n_rows_alloc]; the ESS kernel reads a
   // compact [C][n_cols][rows] copy
@@ -1328,22 +1319,161 @@ int cmc_engine_diagnostics(cmc_engine* e, const cmc_diag_view* o, cmc_error* err
   d.ess_status = fl.p + R;
   CUDA_TRY(launch_diagnostics(d, e->stream));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
-  double* dsts[5] = {o->rhat, o->mean, o->sd, o->ci_lo, o->ci_hi};
-  for (int k = 0; k < 5; ++k)
-    if (dsts[k])
-      CUDA_TRY(cudaMemcpy(dsts[k], out.p + (size_t)k * R, sizeof(double) * R,
-                          cudaMemcpyDeviceToHost));
-  if (o->flags) CUDA_TRY(cudaMemcpy(o->flags, fl.p, sizeof(int) * R, cudaMemcpyDeviceToHost));
-  if (o->ess && e->n_cols)
-    CUDA_TRY(cudaMemcpy(o->ess, out.p + 5 * R, sizeof(double) * e->n_cols,
-                        cudaMemcpyDeviceToHost));
-  if (o->ess_status && e->n_cols)
-    CUDA_TRY(cudaMemcpy(o->ess_status, fl.p + R, sizeof(int) * e->n_cols,
-                        cudaMemcpyDeviceToHost));
+  vals.resize((size_t)5 * R + e->n_cols);
+  flags.resize((size_t)R + e->n_cols);
+  CUDA_TRY(cudaMemcpy(vals.data(), out.p, sizeof(double) * vals.size(), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(flags.data(), fl.p, sizeof(int) * flags.size(), cudaMemcpyDeviceToHost));
   out.free_();
   fl.free_();
   smp.free_();
   return CMC_OK;
+}
+
+static long monitored_count(const cmc_engine* e) {
+  return std::max<long>(0, std::min(e->host_m - 1, e->cfg.burnin + e->cfg.iterations) -
+                               e->cfg.burnin);
+}
+
+int cmc_engine_diagnostics(cmc_engine* e, const cmc_diag_view* o, cmc_error* err) {
+  if (!e || !o || !e->begun) {
+    set_err(err, CMC_ERR_ARG, "diagnostics need a finished run()");
+    return CMC_ERR_ARG;
+  }
+  if (e->C < 2) return fail_config(err, "gelman_rhat needs at least 2 chains");
+  if (e->C > 32) return fail_config(err, "diagnostics support at most 32 chains");
+  if (e->split_tail) {
+    set_err(err, CMC_ERR_ARG, "diagnostics of a sharded engine: gather the shards first");
+    return CMC_ERR_ARG;
+  }
+  const long count = monitored_count(e);
+  if (count < 2) return fail_config(err, "gelman_rhat needs at least 2 iterations");
+  std::vector<double> vals;
+  std::vector<int> flags;
+  int rc = diag_to_host(e, count, vals, flags, err);
+  if (rc) return rc;
+  const long R = 2 + 2 * e->L + e->G * (e->L + 1);
+  double* dsts[5] = {o->rhat, o->mean, o->sd, o->ci_lo, o->ci_hi};
+  for (int k = 0; k < 5; ++k)
+    if (dsts[k]) std::memcpy(dsts[k], vals.data() + (size_t)k * R, sizeof(double) * R);
+  if (o->flags) std::memcpy(o->flags, flags.data(), sizeof(int) * R);
+  if (o->ess && e->n_cols)
+    std::memcpy(o->ess, vals.data() + 5 * R, sizeof(double) * e->n_cols);
+  if (o->ess_status && e->n_cols)
+    std::memcpy(o->ess_status, flags.data() + R, sizeof(int) * e->n_cols);
+  return CMC_OK;
+}
+
+// write_results (P:src/io.cpp:571-720): device diagnostics + host writer.
+int cmc_engine_write_results(cmc_engine* e, const char* outdir, const char* const* genes,
+                             const char* const* contrast_ids, double wall_seconds,
+                             cmc_error* err) {
+  if (!e || !outdir || !e->begun) {
+    set_err(err, CMC_ERR_ARG, "write_results needs a finished run()");
+    return CMC_ERR_ARG;
+  }
+  if (e->split_tail) {
+    set_err(err, CMC_ERR_ARG, "write_results of a sharded engine: gather the shards first");
+    return CMC_ERR_ARG;
+  }
+  if (e->C > 32) return fail_config(err, "diagnostics support at most 32 chains");
+  const long C = e->C, G = e->G, L = e->L;
+  const long count = monitored_count(e);
+  cmc::ResultsInput in;
+  in.outdir = outdir;
+  in.C = C;
+  in.G = G;
+  in.N = e->N;
+  in.L = L;
+  in.genes = genes;
+  in.z = normal_quantile(1.0 - 0.05 / 2.0);
+  // build_diagnostics throws for < 2 chains or < 2 iterations (gelman_rhat,
+  // P:src/diagnostics.cpp:13-15) after the estimate files are written
+  if (C < 2) {
+    in.diag_error = true;
+    in.diag_error_msg = "gelman_rhat needs at least 2 chains";
+  } else if (count < 2) {
+    in.diag_error = true;
+    in.diag_error_msg = "gelman_rhat needs at least 2 iterations";
+  }
+  std::vector<double> vals;
+  std::vector<int> flags;
+  int rc = diag_to_host(e, count, vals, flags, err);
+  if (rc) return rc;
+  const long R = 2 + 2 * L + G * (L + 1);
+  auto part = [&](int k) {
+    return std::vector<double>(vals.begin() + (size_t)k * R, vals.begin() + (size_t)(k + 1) * R);
+  };
+  in.rhat = part(0);
+  in.mean = part(1);
+  in.sd = part(2);
+  in.lo = part(3);
+  in.hi = part(4);
+  in.flags.assign(flags.begin(), flags.begin() + R);
+  in.ess.assign(vals.begin() + 5 * R, vals.end());
+  in.ess_status.assign(flags.begin() + R, flags.end());
+  // thinned-sample columns (engine.cpp:390-400) and each row's column
+  const long nsv = (long)e->saved.size();
+  in.col_names = {"nu", "tau"};
+  for (long l = 0; l < L; ++l) in.col_names.push_back("theta[" + std::to_string(l + 1) + "]");
+  for (long l = 0; l < L; ++l) in.col_names.push_back("sigma[" + std::to_string(l + 1) + "]");
+  in.row_col.assign((size_t)R, -1);
+  for (long r = 0; r < 2 + 2 * L; ++r) in.row_col[(size_t)r] = r;
+  for (long k = 0; k < nsv; ++k) {
+    const long g = e->saved[(size_t)k];
+    for (long l = 0; l < L; ++l) {
+      in.row_col[(size_t)(2 + 2 * L + g * L + l)] = (long)in.col_names.size();
+      in.col_names.push_back("beta[" + std::to_string(g + 1) + "," + std::to_string(l + 1) + "]");
+    }
+    in.row_col[(size_t)(2 + 2 * L + G * L + g)] = (long)in.col_names.size();
+    in.col_names.push_back("gamma[" + std::to_string(g + 1) + "]");
+  }
+  if ((long)in.col_names.size() != e->n_cols) return fail_config(err, "internal: column count");
+  // contrasts
+  if (e->has_ctab) {
+    for (int k = 0; k < e->ctab.n; ++k) {
+      in.contrast_ids.push_back(contrast_ids && contrast_ids[k]
+                                    ? std::string(contrast_ids[k])
+                                    : "contrast" + std::to_string(k + 1));
+      in.per_gene.push_back(e->ctab.per_gene[k]);
+      in.prob_off.push_back(e->ctab.prob_off[k]);
+    }
+    in.n_prob = e->ctab.n_prob;
+    in.probs.resize((size_t)C * in.n_prob);
+    CUDA_TRY(cudaMemcpy(in.probs.data(), e->cprob.p, sizeof(double) * in.probs.size(),
+                        cudaMemcpyDeviceToHost));
+  }
+  // samples: completed rows only
+  in.rows = std::min<long>(e->n_rows, count / e->cfg.thin);
+  in.samples.resize((size_t)C * e->n_cols * in.rows);
+  if (in.rows > 0)
+    CUDA_TRY(cudaMemcpy2D(in.samples.data(), sizeof(double) * in.rows, e->samples.p,
+                          sizeof(double) * e->n_rows, sizeof(double) * in.rows,
+                          (size_t)C * e->n_cols, cudaMemcpyDeviceToHost));
+  for (long r = 0; r < in.rows; ++r) in.sample_iters.push_back(e->cfg.burnin + (r + 1) * e->cfg.thin);
+  // run report
+  in.version = cmc_version();
+  in.seed = e->cfg.seed;
+  in.chains = e->cfg.chains;
+  in.iterations = e->cfg.iterations;
+  in.burnin = e->cfg.burnin;
+  in.tune_cutoff = e->cfg.tune_cutoff;
+  in.thin = e->cfg.thin;
+  in.workers = e->cfg.workers;
+  in.max_step_out = e->cfg.max_step_out;
+  in.save_genes = e->cfg.save_genes;
+  in.slice_faithful = e->cfg.sampler_mode == CMC_SLICE_FAITHFUL;
+  in.wall_seconds = wall_seconds;
+  std::vector<Hyper> hp((size_t)C);
+  CUDA_TRY(cudaMemcpy(hp.data(), e->hyper.p, sizeof(Hyper) * C, cudaMemcpyDeviceToHost));
+  for (long c = 0; c < C; ++c) {
+    // the device sweep is fused: its time is reported under the first step
+    std::vector<double> st(7, 0.0);
+    st[0] = e->sweep_seconds;
+    in.step_seconds.push_back(st);
+    in.clamp_events.push_back(hp[(size_t)c].clamps);
+  }
+  in.saved_genes = e->saved;
+  return cmc::write_results_files(in, err);
 }
 
 // Debug timeline: record warp start/end times of the next `sweeps` sweeps

@@ -377,6 +377,7 @@ class GibbsEngine:
         self.L = spec.X.shape[1]
         self.spec = spec
         self._contrast_specs = [c.finalize() for c in contrasts]
+        self._genes = list(data.genes) if isinstance(data, CountMatrix) and data.genes else None
         self._prob = ProblemArrays(counts, spec.X, spec.h, spec.priors.a,
                                    spec.priors.b, spec.priors.d, spec.priors.c,
                                    spec.priors.s)
@@ -538,6 +539,27 @@ class GibbsEngine:
 
     def run_chain(self, chain: int) -> ChainOutput:
         return self.run()[chain]
+
+    def write_results(self, outdir: str, wall_seconds: float = 0.0,
+                      genes: Optional[Sequence[str]] = None) -> None:
+        """The reference's write_results (P:src/io.cpp:571-720) for the last
+        run(): gene_estimates.csv, hyper_estimates.csv, diagnostics.csv,
+        samples/chain_<c>.csv and run_report.json, from the device-resident
+        accumulators.  Gene labels default to the CountMatrix's."""
+        self.run()
+        labels = list(genes) if genes is not None else self._genes
+        keep = []
+        gl = None
+        if labels is not None:
+            if len(labels) != self.G:
+                raise ConfigError(f"need {self.G} gene labels, got {len(labels)}")
+            keep = [g.encode(errors="surrogateescape") for g in labels]
+            gl = (ctypes.c_char_p * self.G)(*keep)
+        ids = [c.id.encode() for c in self._contrast_specs]
+        cl = (ctypes.c_char_p * max(1, len(ids)))(*ids) if ids else None
+        err = CmcError()
+        _raise(self._lib.cmc_engine_write_results(self._h, str(outdir).encode(), gl, cl,
+                                                  float(wall_seconds), byref(err)), err)
 
     def sample_names(self) -> List[str]:
         L = self.L

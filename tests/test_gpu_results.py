@@ -1,0 +1,178 @@
+"""GPU: results files (CSV emission).  The B200
+engine's write_results (device diagnostics + parallel host formatting) is
+compared file by file with the reference's own write_results
+(P:src/io.cpp:571-720) run on the reference's own ChainOutputs (oracle/_ref).
+
+Every cell is byte-identical except the θ-derived ones (θ rows and θ sample
+columns), which hold to 1e-12 relative: θ's AS241 normal draw goes through
+log.  run_report.json matches key for key; the float layout
+is checked against the reference's nlohmann output on wall_seconds."""
+import csv
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1606_06659_b200 import (ConfigError, ContrastSpec, ContrastTerm, CountMatrix,
+                                   GibbsEngine, ModelSpec, RunConfig, heterosis_contrast,
+                                   parse_param_ref)
+
+from helpers import heterosis
+
+pytestmark = pytest.mark.gpu
+
+
+def _specs(L=5):
+    het = heterosis_contrast(L)
+    het.id = "c1"
+    th = ContrastSpec("c2", [ContrastTerm([(parse_param_ref("theta[2]", L), 1.0)], 0.0)])
+    sg = ContrastSpec("c3", [ContrastTerm([(parse_param_ref("sigma[1]", L), 1.0),
+                                           (parse_param_ref("theta[5]", L), -0.5)], 0.25)])
+    return [het, th, sg]
+
+
+def _labels(G):
+    out = []
+    for g in range(G):
+        if g % 7 == 3:
+            out.append(f"gene,{g}")
+        elif g % 11 == 5:
+            out.append(f'g"{g}"x')
+        else:
+            out.append(f"g{g + 1}")
+    return out
+
+
+def _run_both(tmp_path, G=150, chains=3, burnin=30, iterations=60, thin=5, save=7,
+              wall=1.25, seed=21):
+    counts, X, h = heterosis(G, seed=12)
+    cfg = RunConfig(chains=chains, burnin=burnin, iterations=iterations, thin=thin, seed=seed,
+                    save_genes=save)
+    specs = _specs()
+    genes = _labels(G)
+    eng = GibbsEngine(CountMatrix(counts, genes), ModelSpec(X, h), cfg, contrasts=specs)
+    ref = oracle.RefEngine(counts, X, h, cfg.to_c(), contrasts=[s.flat() for s in specs])
+    a, b = tmp_path / "ours", tmp_path / "ref"
+    return eng, ref, a, b, genes, wall
+
+
+def _fold_int_arrays(text):
+    return re.sub(r"\[\n((?:\s+-?\d+,?\n)+)\s*\]",
+                  lambda m: "[" + ",".join(x.strip().rstrip(",")
+                                           for x in m.group(1).splitlines()) + "]", text)
+
+
+def _theta_cell(name):
+    return "theta[" in name or name.startswith("contrast[c2") or name.startswith("contrast[c3")
+
+
+def _cells_equal(ours, ref, fuzzy):
+    if ours == ref:
+        return True
+    if not fuzzy:
+        return False
+    try:
+        x, y = float(ours), float(ref)
+    except ValueError:
+        return False
+    return x == pytest.approx(y, rel=1e-12, abs=1e-15)
+
+
+def _compare_csv(pa, pb, fuzzy_row=lambda row: False, fuzzy_col=lambda name: False):
+    ra = list(csv.reader(open(pa, newline="")))
+    rb = list(csv.reader(open(pb, newline="")))
+    assert len(ra) == len(rb), pa
+    assert ra[0] == rb[0]
+    header = ra[0]
+    exact_rows = 0
+    for x, y in zip(ra[1:], rb[1:]):
+        assert len(x) == len(y)
+        fr = fuzzy_row(x)
+        for k, (u, v) in enumerate(zip(x, y)):
+            assert _cells_equal(u, v, fr or fuzzy_col(header[k])), (pa, x[0], header[k], u, v)
+        exact_rows += x == y
+    return exact_rows, len(ra) - 1
+
+
+@pytest.mark.usefixtures("ref")
+def test_results_files_match_reference(tmp_path):
+    eng, ref, a, b, genes, wall = _run_both(tmp_path)
+    eng.write_results(str(a), wall_seconds=wall)
+    ref.write_results(str(b), genes=genes, wall_seconds=wall)
+    # gene estimates: every byte
+    assert open(a / "gene_estimates.csv", "rb").read() == open(b / "gene_estimates.csv", "rb").read()
+    # hyper estimates and diagnostics: byte-identical except theta-derived rows
+    ex, n = _compare_csv(a / "hyper_estimates.csv", b / "hyper_estimates.csv",
+                         fuzzy_row=lambda row: _theta_cell(row[0]))
+    assert ex >= n - 5 - 2
+    ex, n = _compare_csv(a / "diagnostics.csv", b / "diagnostics.csv",
+                         fuzzy_row=lambda row: _theta_cell(row[0]))
+    assert ex >= n - 5
+    for c in range(1, 4):
+        f = f"samples/chain_{c}.csv"
+        _compare_csv(a / f, b / f, fuzzy_col=_theta_cell)
+    ja, jb = json.load(open(a / "run_report.json")), json.load(open(b / "run_report.json"))
+    assert set(ja) == set(jb)
+    for k in ja:
+        if k in ("version", "step_seconds"):
+            continue
+        if k == "per_chain":
+            for x, y in zip(ja[k], jb[k]):
+                assert x["chain"] == y["chain"] and x["clamp_events"] == y["clamp_events"]
+                assert set(x["step_seconds"]) == set(y["step_seconds"])
+            continue
+        assert ja[k] == jb[k], k
+    # layout: identical lines wherever the values are.  The oracle build's
+    # json.hpp is cudnn_frontend's copy, locally modified to print integer
+    # arrays inline; stock nlohmann (vendored by the reference upstream)
+    # prints one element per line, as we do, so fold ours before comparing.
+    la = _fold_int_arrays(open(a / "run_report.json").read()).splitlines()
+    lb = open(b / "run_report.json").read().splitlines()
+    assert len(la) == len(lb)
+    same = [x == y for x, y in zip(la, lb)]
+    assert sum(same) >= len(la) - 2 - 7 - 7 * 3  # version + step_seconds values
+
+
+@pytest.mark.usefixtures("ref")
+@pytest.mark.parametrize("wall", [0.0, 1.25, 1e-05, 0.000123, 123456.0, 0.1, 2.5e20,
+                                  1234567890123456.0, 12345678901234567890.0, 7.0])
+def test_report_float_layout(tmp_path, wall):
+    eng, ref, a, b, genes, _ = _run_both(tmp_path, G=40, chains=2, burnin=10, iterations=10,
+                                         thin=5, save=2)
+    eng.write_results(str(a), wall_seconds=wall)
+    ref.write_results(str(b), genes=genes, wall_seconds=wall)
+    wa = [x for x in open(a / "run_report.json") if '"wall_seconds"' in x]
+    wb = [x for x in open(b / "run_report.json") if '"wall_seconds"' in x]
+    assert wa == wb
+
+
+@pytest.mark.usefixtures("ref")
+def test_single_chain_writes_estimates_then_raises(tmp_path):
+    eng, ref, a, b, genes, wall = _run_both(tmp_path, G=60, chains=1, burnin=10, iterations=20)
+    with pytest.raises(ConfigError) as e1:
+        eng.write_results(str(a), wall_seconds=wall)
+    with pytest.raises(oracle.ConfigErr) as e2:
+        ref.write_results(str(b), genes=genes, wall_seconds=wall)
+    assert str(e1.value) == str(e2.value)
+    for f in ("gene_estimates.csv", "diagnostics.csv"):
+        assert open(a / f, "rb").read() == open(b / f, "rb").read()
+    _compare_csv(a / "hyper_estimates.csv", b / "hyper_estimates.csv",
+                 fuzzy_row=lambda row: _theta_cell(row[0]))
+
+
+def test_default_labels_and_bad_outdir(tmp_path):
+    counts, X, h = heterosis(64, seed=3)
+    eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, h),
+                      RunConfig(chains=2, burnin=10, iterations=20, thin=5, seed=1))
+    eng.write_results(str(tmp_path / "o"))
+    rows = list(csv.reader(open(tmp_path / "o" / "gene_estimates.csv")))
+    assert [r[0] for r in rows[1:4]] == ["g1", "g2", "g3"]
+    assert len(rows) == 65 and len(rows[0]) == 1 + 4 * 5 + 4
+    d = list(csv.reader(open(tmp_path / "o" / "diagnostics.csv")))
+    assert len(d) == 1 + 2 + 10 + 64 * 6
+    (tmp_path / "file").write_text("x")
+    with pytest.raises(ConfigError, match="cannot create output directory"):
+        eng.write_results(str(tmp_path / "file" / "sub"))
