@@ -1,13 +1,14 @@
 // C++ caller of the B200 engine through include/countmc_b200.hpp, written
 // the way a user of countmc::GibbsEngine writes it.  Deterministic inputs;
 // prints one JSON line that tests/test_gpu_facade.py compares with the
-// Python mirror on the same inputs.
+// Python mirror on the same inputs.  With an argument, also writes the
+// reference's result files there.
 #include <cmath>
 #include <cstdio>
 
 #include "countmc_b200.hpp"
 
-int main() {
+int main(int argc, char** argv) {
   using namespace countmc_b200;
   Problem p;
   p.G = 300;
@@ -40,6 +41,7 @@ int main() {
     std::uint64_t clamps = 0;
     eng.iterate(st, tu, 1, 1, &clamps);
     auto outs = eng.run();
+    if (argc > 1) eng.write_results(argv[1]);  // the reference's result files
     double bsum = 0.0;
     for (long i = 2 + 2 * p.L; i < 2 + 2 * p.L + p.G * p.L; ++i) bsum += outs[0].mean[i];
     std::printf("{\"iter_nu\": %.17g, \"iter_eps0\": %.17g, \"nu0\": %.17g, \"nu1\": %.17g, "

@@ -235,6 +235,20 @@ class GibbsEngine {
   }
 
   // GibbsEngine::run: every chain, batched on the device.
+  // write_results (P:src/io.cpp:571-720) for the last run(); labels and ids
+  // may be empty ("g<g+1>" / "contrast<k>").
+  void write_results(const std::string& outdir, const std::vector<std::string>& genes = {},
+                     const std::vector<std::string>& contrast_ids = {},
+                     double wall_seconds = 0.0) {
+    std::vector<const char*> g, c;
+    for (const auto& s : genes) g.push_back(s.c_str());
+    for (const auto& s : contrast_ids) c.push_back(s.c_str());
+    cmc_error e{};
+    check(cmc_engine_write_results(h_, outdir.c_str(), g.empty() ? nullptr : g.data(),
+                                   c.empty() ? nullptr : c.data(), wall_seconds, &e),
+          e);
+  }
+
   std::vector<ChainOutput> run() {
     cmc_error e{};
     check(cmc_engine_begin(h_, &e), e);

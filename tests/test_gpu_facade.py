@@ -15,9 +15,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_cpp_facade_matches_python_mirror():
+def test_cpp_facade_matches_python_mirror(tmp_path):
     exe = os.path.join(ROOT, "paper_1606_06659_b200", "lib", "facade_run")
-    out = json.loads(subprocess.run([exe], check=True, capture_output=True,
+    out = json.loads(subprocess.run([exe, str(tmp_path / "cpp")], check=True, capture_output=True,
                                     text=True).stdout.strip().splitlines()[-1])
     G, N, L = 300, 16, 5
     X = builtin_design("heterosis16x5", N)
@@ -34,3 +34,7 @@ def test_cpp_facade_matches_python_mirror():
     for v in outs[0].beta_acc.mean.ravel():
         bsum += float(v)
     assert out["beta_mean_sum"] == bsum and out["count"] == 60
+    eng.write_results(str(tmp_path / "py"))
+    for f in ("gene_estimates.csv", "hyper_estimates.csv", "diagnostics.csv",
+              "samples/chain_1.csv", "samples/chain_2.csv"):
+        assert (tmp_path / "cpp" / f).read_bytes() == (tmp_path / "py" / f).read_bytes(), f
