@@ -37,7 +37,22 @@ __device__ __forceinline__ void exp_table_init(double* tab) {
   if (threadIdx.x < 32) tab[threadIdx.x] = g_exp_table[threadIdx.x];
 }
 
-__device__ __forceinline__ double fast_exp_le700(double x, const double* tab) {
+// The block's table by its 32-bit shared-window address, converted once per
+// thread: loads are then a plain ld.shared (no generic-to-shared
+// conversion per call inside the slice loops).
+struct ExpTab {
+  unsigned s;
+  ExpTab() = default;
+  __device__ __forceinline__ explicit ExpTab(const double* tab)
+      : s((unsigned)__cvta_generic_to_shared(tab)) {}
+  __device__ __forceinline__ double operator[](int j) const {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(s + ((unsigned)j << 3)));
+    return v;
+  }
+};
+
+__device__ __forceinline__ double fast_exp_le700(double x, const ExpTab tab) {
   if (x < -707.0) return exp(x);
   const double t = fma(x, kExpC[0], kExpC[1]);
   const int k = __double2loint(t);
@@ -54,7 +69,7 @@ __device__ __forceinline__ double fast_exp_le700(double x, const double* tab) {
   return __hiloint2double(__double2hiint(res) + ((k >> 5) << 20), __double2loint(res));
 }
 
-__device__ __forceinline__ double fast_exp(double x, const double* tab) {
+__device__ __forceinline__ double fast_exp(double x, const ExpTab tab) {
   if (x > 700.0) return exp(x);
   return fast_exp_le700(x, tab);
 }

@@ -180,7 +180,7 @@ __device__ __forceinline__ double slice_step_so2(F& f, double x0, double& w,
 // :13-19): y*e - exp(min(h + eta + e, 700)) - e*e / (2 gamma).
 struct EpsF {
   double y, cn, inv_two_gam, e700;
-  const double* tab;
+  ExpTab tab;
   unsigned clamps;
   double EL, ER, rL, rR;  // step-out: exp(cn + lo), exp(cn + hi), exp(-w), exp(w)
   __device__ __forceinline__ double operator()(double x) {
@@ -260,7 +260,7 @@ struct BetaF {
   const double* val;   // group values (uniform across the warp)
   const double* S;     // shared memory, stride kGeneBlock
   const double* logS;
-  const double* tab;
+  ExpTab tab;
   int J;
   unsigned clamps;
   __device__ __forceinline__ double operator()(double b) {
@@ -274,6 +274,33 @@ struct BetaF {
         tot -= e700;
       } else if (Sj > 0.0) {
         tot -= Sj * fast_exp(t, tab);
+      }
+    }
+    const double zz = b - theta;
+    return tot - zz * zz * inv_two_sig2;
+  }
+};
+
+// BetaF with the (at most JR) group sums in registers: same terms in the
+// same order; each term is branch-free (the clamp and S_j = 0 cases select
+// their value), which keeps the slice loop's evaluation straight-line.
+template <int JR>
+struct BetaFR {
+  double a, theta, inv_two_sig2, e700;
+  double v[JR], S[JR], lS[JR];
+  ExpTab tab;
+  int J;
+  unsigned clamps;
+  __device__ __forceinline__ double operator()(double b) {
+    double tot = a * b;
+#pragma unroll
+    for (int j = 0; j < JR; ++j) {
+      if (j < J) {
+        const double t = v[j] * b;
+        const bool cl = lS[j] + t > kExpClamp;
+        const double e = fast_exp(t, tab);
+        clamps += cl ? 1u : 0u;
+        tot -= cl ? e700 : (S[j] > 0.0 ? S[j] * e : 0.0);
       }
     }
     const double zz = b - theta;
@@ -443,7 +470,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   double xb = 0.0;
   for (int l = 0; l < L; ++l) xb += __ldg(p.X + n * L + l) * beta[(size_t)l * G + gl];
   const double inv_two_gam = 1.0 / (2.0 * p.gam[so * G + gl]);
-  EpsF f{__ldg(p.y + i), __ldg(p.h + n) + xb, inv_two_gam, p.exp_clamp, exp_tab, 0u};
+  EpsF f{__ldg(p.y + i), __ldg(p.h + n) + xb, inv_two_gam, p.exp_clamp, ExpTab(exp_tab), 0u};
   const double x0 = p.eps[ie];
   double w = p.eps_w[ie];
   double wa = tuning ? p.eps_wa[ie] : 0.0;
@@ -477,12 +504,16 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 #ifndef CMC_GENE_MIN_BLOCKS
 #define CMC_GENE_MIN_BLOCKS 5
 #endif
+// JR > 0: every column has at most JR groups, kept in registers
+// (BetaFR); JR = 0: any design, group sums in shared memory (BetaF).
+template <int JR>
 __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
     gene_sweep_kernel(const SweepParams p, const long m_off) {
   extern __shared__ double smem[];
   __shared__ double exp_tab[32];
   exp_table_init(exp_tab);
   __syncthreads();
+  const ExpTab etab(exp_tab);
   WarpTrace wt(p, 2, p.slot_base + blockIdx.y);
   const int tid = threadIdx.x;
   const int slot = p.slot_base + blockIdx.y;
@@ -577,32 +608,64 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
     __syncwarp();
     if (alive) {
       bold = beta[i];
-      for (int j = jb; j < je; ++j) {
+      // S_j = sum over the group's samples, in order, of
+      // clamped_exp(lp_n - v_j * bold) (P:src/engine.cpp:295-300)
+      auto group_sum = [&](int j) {
         const double v = __ldg(p.grp_val + j);
+        const double vb = v * bold;
+        const int q0 = __ldg(p.grp_moff + j), q1 = __ldg(p.grp_moff + j + 1);
         double s = 0.0;
-        for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
+        for (int q = q0; q < q1; ++q) {
           const int n = __ldg(p.grp_mem + q);
-          double t = xs[n * kGeneBlock + tid] - v * bold;
+          double t = xs[n * kGeneBlock + tid] - vb;
           if (t > kExpClamp) {
             ++clamps;
             t = kExpClamp;
           }
-          s += fast_exp(t, exp_tab);
+          s += fast_exp(t, etab);
         }
-        sS[(j - jb) * kGeneBlock + tid] = s;
-        sLogS[(j - jb) * kGeneBlock + tid] = log(s);
-      }
+        return s;
+      };
       const double sig = hp->sigma[l];
       const double sig2 = sig * sig;
-      BetaF f{__ldg(p.A + i), hp->theta[l], 1.0 / (2.0 * sig2), p.exp_clamp,
-              p.grp_val + jb, sS + tid, sLogS + tid, exp_tab, je - jb, 0u};
       w0 = beta_w[i];
       w = w0;
       wa = tuning ? beta_wa[i] : 0.0;
       Stream rng;
       rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l));
-      bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
-      clamps += f.clamps;
+      if constexpr (JR > 0) {
+        BetaFR<JR> f;
+        f.a = __ldg(p.A + i);
+        f.theta = hp->theta[l];
+        f.inv_two_sig2 = 1.0 / (2.0 * sig2);
+        f.e700 = p.exp_clamp;
+        f.tab = etab;
+        f.J = je - jb;
+        f.clamps = 0u;
+#pragma unroll
+        for (int jj = 0; jj < JR; ++jj) {
+          f.v[jj] = 0.0;
+          f.S[jj] = 0.0;
+          f.lS[jj] = 0.0;
+          if (jb + jj < je) {
+            f.v[jj] = __ldg(p.grp_val + jb + jj);
+            f.S[jj] = group_sum(jb + jj);
+            f.lS[jj] = log(f.S[jj]);
+          }
+        }
+        bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
+        clamps += f.clamps;
+      } else {
+        for (int j = jb; j < je; ++j) {
+          const double s = group_sum(j);
+          sS[(j - jb) * kGeneBlock + tid] = s;
+          sLogS[(j - jb) * kGeneBlock + tid] = log(s);
+        }
+        BetaF f{__ldg(p.A + i), hp->theta[l], 1.0 / (2.0 * sig2), p.exp_clamp,
+                p.grp_val + jb, sS + tid, sLogS + tid, etab, je - jb, 0u};
+        bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
+        clamps += f.clamps;
+      }
     }
     __syncwarp();
     if (!alive) continue;
@@ -1036,18 +1099,26 @@ cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
   return launch_prio(eps_sweep_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_eps, p, m_off);
 }
 
-cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
-                              cudaStream_t s) {
-  const int smem = gene_sweep_smem_bytes(p.N, p.Jmax);
+template <int JR>
+static cudaError_t launch_gene_sweep_t(const SweepParams& p, int chains, long m_off,
+                                       cudaStream_t s) {
+  const int smem = gene_sweep_smem_bytes(p.N, JR > 0 ? 0 : p.Jmax);
   static int configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(
-        gene_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        gene_sweep_kernel<JR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)chains);
-  return launch_prio(gene_sweep_kernel, grid, dim3(kGeneBlock), smem, s, p.prio_gene, p, m_off);
+  return launch_prio(gene_sweep_kernel<JR>, grid, dim3(kGeneBlock), smem, s, p.prio_gene, p,
+                     m_off);
+}
+
+cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
+                              cudaStream_t s) {
+  if (p.Jmax <= 2) return launch_gene_sweep_t<2>(p, chains, m_off, s);
+  return launch_gene_sweep_t<0>(p, chains, m_off, s);
 }
 
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
