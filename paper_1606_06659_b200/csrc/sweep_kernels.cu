@@ -437,10 +437,12 @@ __device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
 // independent given the gene's previous beta and gamma (P:src/engine.cpp:
 // 178-202), so the 16 slice steps of a gene run on 16 threads.  A warp holds
 // 32 consecutive genes at one sample n (coalesced SoA loads), the grid's y
-// dimension is n and z the chain.  Everything a step needs fits in
-// registers, so occupancy is high and the tail wave is short.
+// dimension is n and z the chain.  Capped at 64 registers (8 blocks, 32
+// warps per SM; one 8-byte spill): the step is latency-bound, and the extra
+// warps beat the spill (A/B on B200: 6 blocks 4.18e8, 8 blocks 4.31e8
+// gene-iter/s, 9-10 blocks no better once the gene kernel also runs at 6).
 #ifndef CMC_EPS_MIN_BLOCKS
-#define CMC_EPS_MIN_BLOCKS 6
+#define CMC_EPS_MIN_BLOCKS 8
 #endif
 __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
     eps_sweep_kernel(const SweepParams p, const long m_off) {
@@ -500,9 +502,10 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 // beta_g1..beta_gL in column order.  Lanes of a warp are re-converged with
 // __syncwarp() at every slice-step boundary so each step's log-density
 // evaluations run as one SIMT stream (no early exits: a lane without a
-// gene, or whose gene stalled, idles with alive == false).
+// gene, or whose gene stalled, idles with alive == false).  6 blocks per
+// SM (80 registers, small spills) measured best with the eps kernel at 8.
 #ifndef CMC_GENE_MIN_BLOCKS
-#define CMC_GENE_MIN_BLOCKS 5
+#define CMC_GENE_MIN_BLOCKS 6
 #endif
 // JR > 0: every column has at most JR groups, kept in registers
 // (BetaFR); JR = 0: any design, group sums in shared memory (BetaF).
