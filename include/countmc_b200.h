@@ -83,7 +83,25 @@ typedef struct cmc_problem {
   double d;
   const double* c;
   const double* s;
+  /* Optional xi-augmented beta priors (SURVEY.md section 8(f) rank 4,
+   * BASELINE configs 2-3).  NOT in the reference -- parity unpinned; the
+   * parameterisation is DESIGN.md section 7's:
+   *   beta_gl ~ N(theta_l, sigma_l^2 xi_gl),  xi_gl ~ prior_l, with
+   *   NORMAL xi = 1, LAPLACE xi ~ Exp(rate 1/2), T xi ~ IG(k/2, k/2),
+   *   HORSESHOE sqrt(xi) ~ Cauchy+(0, 1).
+   * beta_prior: L entries, NULL = all normal (the reference model).
+   * t_df: k of the t prior (> 0 when any column is T).  With any non-normal
+   * column the packed layouts gain a trailing xi block of G x L entries:
+   * state [... | tau | xi], tuning [... | tau | xi], accumulators
+   * [... | eps | xi]. */
+  const int* beta_prior;
+  double t_df;
 } cmc_problem;
+
+#define CMC_PRIOR_NORMAL 0
+#define CMC_PRIOR_LAPLACE 1
+#define CMC_PRIOR_T 2
+#define CMC_PRIOR_HORSESHOE 3
 
 /* RunConfig (engine.hpp:21-36) with SliceConfig (slice.hpp:11-17) inlined.
  * tune_cutoff < 0 resolves to min(500, burnin/10) (engine.cpp:33). */

@@ -71,6 +71,8 @@ def load_oracle():
     lib.orc_log_fc_sigma.restype = c_double
     lib.orc_tune_update.argtypes = [D, D, c_long, c_double, c_void_p]
     lib.orc_slice_chain.argtypes = [c_int, c_double, c_long, c_long, c_double, c_uint64, D]
+    lib.orc_log_fc_xi.argtypes = [c_int, c_double, c_double, c_double]
+    lib.orc_log_fc_xi.restype = c_double
     lib.orc_pairwise_sum.argtypes = [D, ctypes.c_size_t]
     lib.orc_pairwise_sum.restype = c_double
     lib.orc_det_sum.argtypes = [D, c_long]
@@ -170,8 +172,8 @@ def _check(rc, err):
     raise RuntimeError(err.msg.decode())
 
 
-def new_outputs(G, N, L, n_saved, n_rows, n_prob, n_contrasts):
-    S, _, A = sizes(G, N, L)
+def new_outputs(G, N, L, n_saved, n_rows, n_prob, n_contrasts, xi=False):
+    S, _, A = sizes(G, N, L, xi)
     ncols = 2 + 2 * L + n_saved * (L + 1)
     o = dict(count=np.zeros(1, np.int64), mean=np.zeros(A), meansq=np.zeros(A),
              mean_c=np.zeros(A), meansq_c=np.zeros(A), prob=np.zeros(max(1, n_prob)),
@@ -195,7 +197,9 @@ class _Base:
         self.cfg = cfg
         self.prob = ProblemArrays(counts, X, h, pr.get("a", 1.0), pr.get("b", 1.0),
                                   pr.get("d", 1000.0), pr.get("c", [10.0] * L),
-                                  pr.get("s", [100.0] * L))
+                                  pr.get("s", [100.0] * L), pr.get("beta_prior"),
+                                  pr.get("t_df", 1.0))
+        self.xi = self.prob.xi
         self.contrasts = list(contrasts)
         self.ctr = ContrastArrays(self.contrasts)
 
@@ -227,7 +231,7 @@ class OracleEngine(_Base):
         return out[:n]
 
     def initial_state(self, chain):
-        S, _, _ = sizes(self.G, self.N, self.L)
+        S, _, _ = sizes(self.G, self.N, self.L, self.xi)
         st = np.zeros(S)
         self.lib.orc_initial_state(self.h, chain, dptr(st))
         return st
@@ -245,7 +249,7 @@ class OracleEngine(_Base):
                      else 1 for c in self.contrasts)
         n_rows = self.resolved.iterations // self.resolved.thin
         o, view = new_outputs(self.G, self.N, self.L, len(self.saved_genes()), n_rows, n_prob,
-                              len(self.contrasts))
+                              len(self.contrasts), self.xi)
         err = CmcError()
         _check(self.lib.orc_run_chain(self.h, chain, byref(view), byref(err)), err)
         return o

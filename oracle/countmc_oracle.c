@@ -253,6 +253,26 @@ double orc_log_fc_sigma(double sigma, long G, double ss, double s_bound) {
   return -(double)G * log(sigma) - ss / (2.0 * sigma * sigma);
 }
 
+/* xi full conditional (extension, no reference: parity unpinned).  With
+ * q = (beta - theta)^2 / (2 sigma^2) and beta ~ N(theta, sigma^2 xi):
+ *   laplace   xi ~ Exp(rate 1/2):        -log(xi)/2 - q/xi - xi/2
+ *   t(k)      xi ~ IG(k/2, k/2):         -(k/2 + 3/2) log(xi) - (q + k/2)/xi
+ *   horseshoe sqrt(xi) ~ Cauchy+(0,1):   -log(xi) - q/xi - log1p(xi)
+ * and -inf for xi <= 0. */
+double orc_log_fc_xi(int prior, double xi, double q, double k) {
+  if (!(xi > 0.0)) return -INFINITY;
+  switch (prior) {
+    case CMC_PRIOR_LAPLACE:
+      return -0.5 * log(xi) - q / xi - 0.5 * xi;
+    case CMC_PRIOR_T:
+      return -(0.5 * k + 1.5) * log(xi) - (q + 0.5 * k) / xi;
+    case CMC_PRIOR_HORSESHOE:
+      return -log(xi) - q / xi - log1p(xi);
+    default:
+      return 0.0;
+  }
+}
+
 /* ---------------------------------------------------------------- slice */
 
 /* P:include/countmc/slice.hpp:27-35 */
@@ -316,6 +336,19 @@ static double d_box(void* c, double x) {
   (void)c;
   return (x > 0.0 && x < 1.0) ? 0.0 : -INFINITY;
 }
+/* xi conditionals at q = 0.7 (t: k = 3, i.e. IG(2, 2.2)) */
+static double d_xi_t(void* c, double x) {
+  (void)c;
+  return orc_log_fc_xi(CMC_PRIOR_T, x, 0.7, 3.0);
+}
+static double d_xi_laplace(void* c, double x) {
+  (void)c;
+  return orc_log_fc_xi(CMC_PRIOR_LAPLACE, x, 0.7, 0.0);
+}
+static double d_xi_horseshoe(void* c, double x) {
+  (void)c;
+  return orc_log_fc_xi(CMC_PRIOR_HORSESHOE, x, 0.7, 0.0);
+}
 
 /* run_chain helper of P:tests/test_slice.cpp:21-39. */
 int orc_slice_chain(int density, double x0, long n, long burnin,
@@ -323,7 +356,10 @@ int orc_slice_chain(int density, double x0, long n, long burnin,
   orc_logf f = density == 0   ? d_normal
                : density == 1 ? d_gamma32
                : density == 2 ? d_invgamma23
-                              : d_box;
+               : density == 3 ? d_box
+               : density == 4 ? d_xi_t
+               : density == 5 ? d_xi_laplace
+                              : d_xi_horseshoe;
   orc_slice_cfg cfg = {100, burnin, burnin / 10, w_init, 1000};
   double w = w_init, waux = 0.0, x = x0;
   long k = 0;
@@ -403,7 +439,7 @@ double orc_disjunction_combine(double p1, double p2, double p12) {
 
 /* Draw-site families, P:include/countmc/engine.hpp:42-49 */
 enum { kEps = 1, kGamma = 2, kNu = 3, kTau = 4, kBeta = 5, kTheta = 6,
-       kSigma = 7, kSaveSel = 8 };
+       kSigma = 7, kSaveSel = 8, kXi = 11 /* extension: xi priors */ };
 static uint64_t site_id(uint64_t fam, uint64_t flat) {
   return (fam << 56) | flat;
 }
@@ -441,6 +477,10 @@ struct orc_engine {
   long* saved;
   int n_contrasts;
   orc_contrast* contrasts;
+  /* xi-augmented beta priors (extension, no reference: parity unpinned) */
+  int xi_any;
+  int* prior; /* L: CMC_PRIOR_* */
+  double t_df;
 };
 
 static void set_err(cmc_error* err, int code, const char* msg) {
@@ -553,6 +593,17 @@ int orc_engine_create(const cmc_problem* p, const cmc_run_config* cfg_in,
       set_err(err, CMC_ERR_CONFIG, "prior entries c, s must be strictly positive");
       return CMC_ERR_CONFIG;
     }
+  if (p->beta_prior)
+    for (long l = 0; l < p->L; ++l) {
+      if (p->beta_prior[l] < CMC_PRIOR_NORMAL || p->beta_prior[l] > CMC_PRIOR_HORSESHOE) {
+        set_err(err, CMC_ERR_CONFIG, "beta prior must be normal, laplace, t or horseshoe");
+        return CMC_ERR_CONFIG;
+      }
+      if (p->beta_prior[l] == CMC_PRIOR_T && !(p->t_df > 0.0)) {
+        set_err(err, CMC_ERR_CONFIG, "t prior needs positive degrees of freedom");
+        return CMC_ERR_CONFIG;
+      }
+    }
   cmc_run_config cfg = *cfg_in;
   const char* bad = NULL;
   if (cfg.chains < 1) bad = "chains must be >= 1";
@@ -593,6 +644,10 @@ int orc_engine_create(const cmc_problem* p, const cmc_run_config* cfg_in,
   e->s = (double*)malloc(sizeof(double) * (size_t)L);
   memcpy(e->c, p->c, sizeof(double) * (size_t)L);
   memcpy(e->s, p->s, sizeof(double) * (size_t)L);
+  e->prior = (int*)calloc((size_t)L, sizeof(int));
+  if (p->beta_prior) memcpy(e->prior, p->beta_prior, sizeof(int) * (size_t)L);
+  for (long l = 0; l < L; ++l) e->xi_any |= e->prior[l] != CMC_PRIOR_NORMAL;
+  e->t_df = p->t_df;
   e->cfg = cfg;
   e->scfg.max_step_out = cfg.max_step_out;
   e->scfg.burnin = cfg.burnin;
@@ -700,6 +755,7 @@ void orc_engine_destroy(orc_engine* e) {
   free(e->h);
   free(e->c);
   free(e->s);
+  free(e->prior);
   free(e->A);
   if (e->groups) {
     for (long l = 0; l < e->L; ++l) {
@@ -751,6 +807,8 @@ int orc_engine_saved_genes(const orc_engine* e, long* out) {
 #define TU_SIGMA(e) (TU_BETA(e) + (e)->G * (e)->L)
 #define TU_NU(e) (TU_SIGMA(e) + (e)->L)
 #define TU_TAU(e) (TU_NU(e) + 1)
+#define ST_XI(e) (ST_TAU(e) + 1)
+#define TU_XI(e) (TU_TAU(e) + 1)
 
 static double std_max(double a, double b) { return (a < b) ? b : a; }
 static double std_min(double a, double b) { return (b < a) ? b : a; }
@@ -772,6 +830,8 @@ int orc_initial_state(const orc_engine* e, long chain, double* st) {
   }
   st[ST_NU(e)] = 2.0;
   st[ST_TAU(e)] = 1.0;
+  if (e->xi_any)
+    for (long i = 0; i < G * L; ++i) st[ST_XI(e) + i] = 1.0;
 
   double hbar = 0.0;
   for (long n = 0; n < N; ++n) hbar += e->h[n];
@@ -853,6 +913,7 @@ static double f_sig(void* c, double v) {
 /* grouped beta density, P:src/engine.cpp:303-316 */
 typedef struct {
   double a, theta, sig2;
+  double xi; /* > 0: xi column, prior variance sig2 * xi (extension) */
   long J;
   const orc_group* groups;
   const double* S;
@@ -872,7 +933,16 @@ static double f_beta(void* c, double b) {
     }
   }
   const double zz = b - k->theta;
+  if (k->xi > 0.0) return tot - zz * zz / (2.0 * (k->sig2 * k->xi));
   return tot - zz * zz / (2.0 * k->sig2);
+}
+typedef struct {
+  int prior;
+  double q, k;
+} xi_ctx;
+static double f_xi(void* c, double x) {
+  xi_ctx* k = (xi_ctx*)c;
+  return orc_log_fc_xi(k->prior, x, k->q, k->k);
 }
 
 /* GibbsEngine::iterate, P:src/engine.cpp:161-370, executed sequentially
@@ -890,6 +960,7 @@ int orc_iterate(const orc_engine* e, double* st, double* tw, double* ta,
   double* sigma = st + ST_SIGMA(e);
   double* nu = st + ST_NU(e);
   double* tau = st + ST_TAU(e);
+  double* xi = e->xi_any ? st + ST_XI(e) : NULL;
   double* xb = (double*)malloc(sizeof(double) * (size_t)(G * N));
   double* lp = (double*)malloc(sizeof(double) * (size_t)(G * N));
   double* tmp = (double*)malloc(sizeof(double) * (size_t)G);
@@ -1003,7 +1074,9 @@ int orc_iterate(const orc_engine* e, double* st, double* tw, double* ta,
         Sp[j] = sacc;
         logSp[j] = log(sacc);
       }
-      beta_ctx k = {e->A[g * L + l], theta_l, sig2, J, grp, Sp, logSp, clamps};
+      const int xcol = e->prior[l] != CMC_PRIOR_NORMAL;
+      beta_ctx k = {e->A[g * L + l], theta_l, sig2, xcol ? xi[g * L + l] : 0.0,
+                    J, grp, Sp, logSp, clamps};
       orc_stream rng;
       orc_stream_init(&rng, seed, ch, it, site_id(kBeta, (uint64_t)(g * L + l)));
       const double wv = tw[TU_BETA(e) + g * L + l];
@@ -1020,6 +1093,22 @@ int orc_iterate(const orc_engine* e, double* st, double* tw, double* ta,
         for (long j = 0; j < J; ++j)
           for (long q = 0; q < grp[j].n_idx; ++q)
             lpg[grp[j].idx[q]] += grp[j].value * (bnew - bold);
+      if (xcol) {
+        /* xi_gl right after beta_gl (extension; its conditional reads only
+         * beta_gl, theta_l and sigma_l of iteration m-1) */
+        const double dz = bnew - theta_l;
+        xi_ctx kx = {e->prior[l], dz * dz / (2.0 * sig2), e->t_df};
+        orc_stream rx;
+        orc_stream_init(&rx, seed, ch, it, site_id(kXi, (uint64_t)(g * L + l)));
+        const double x0 = xi[g * L + l], wx = tw[TU_XI(e) + g * L + l];
+        xi[g * L + l] = orc_slice_step(f_xi, &kx, x0, &tw[TU_XI(e) + g * L + l],
+                                       &ta[TU_XI(e) + g * L + l], sc, m, &rx, &stalled);
+        if (stalled) {
+          set_stall(err, "xi", g + 1, l + 1, x0, wx, m);
+          rc = CMC_ERR_STALL;
+          break;
+        }
+      }
     }
     if (J > 64) {
       free(Sp);
@@ -1030,10 +1119,23 @@ int orc_iterate(const orc_engine* e, double* st, double* tw, double* ta,
 
   /* Step 6: theta, P:src/engine.cpp:336-347 */
   for (long l = 0; l < L; ++l) {
-    for (long g = 0; g < G; ++g) tmp[g] = beta[g * L + l];
-    const double sb = orc_det_sum(tmp, G);
     double mean, sd;
-    orc_theta_fc_params(sb, G, sigma[l], e->c[l], &mean, &sd);
+    if (e->prior[l] != CMC_PRIOR_NORMAL) {
+      /* extension: precision 1/c^2 + sum_g 1/(sigma^2 xi_g), mean from
+       * sum_g beta_g / xi_g */
+      for (long g = 0; g < G; ++g) tmp[g] = 1.0 / xi[g * L + l];
+      const double sw = orc_det_sum(tmp, G);
+      for (long g = 0; g < G; ++g) tmp[g] = beta[g * L + l] / xi[g * L + l];
+      const double sbw = orc_det_sum(tmp, G);
+      const double sg = sigma[l], cl = e->c[l];
+      const double v = 1.0 / (1.0 / (cl * cl) + sw / (sg * sg));
+      mean = v * sbw / (sg * sg);
+      sd = sqrt(v);
+    } else {
+      for (long g = 0; g < G; ++g) tmp[g] = beta[g * L + l];
+      const double sb = orc_det_sum(tmp, G);
+      orc_theta_fc_params(sb, G, sigma[l], e->c[l], &mean, &sd);
+    }
     orc_stream rng;
     orc_stream_init(&rng, seed, ch, it, site_id(kTheta, (uint64_t)l));
     theta[l] = mean + sd * orc_normal(&rng);
@@ -1042,9 +1144,10 @@ int orc_iterate(const orc_engine* e, double* st, double* tw, double* ta,
   /* Step 7: sigma, P:src/engine.cpp:349-369 */
   for (long l = 0; l < L; ++l) {
     const double th = theta[l];
+    const int xcol = e->prior[l] != CMC_PRIOR_NORMAL;
     for (long g = 0; g < G; ++g) {
       const double dlt = beta[g * L + l] - th;
-      tmp[g] = dlt * dlt;
+      tmp[g] = xcol ? dlt * dlt / xi[g * L + l] : dlt * dlt;
     }
     sig_ctx k = {G, orc_det_sum(tmp, G), e->s[l]};
     orc_stream rng;
@@ -1084,9 +1187,10 @@ static double param_value(const orc_engine* e, const double* st, int fam,
 int orc_run_chain(const orc_engine* e, long chain, const cmc_output_view* out,
                   cmc_error* err) {
   const long G = e->G, N = e->N, L = e->L;
-  const long S = G * N + G + G * L + 2 * L + 2;
-  const long T = G * N + G + G * L + L + 2;
-  const long A = 2 + 2 * L + G * L + G + G * N;
+  const long XI = e->xi_any ? G * L : 0;
+  const long S = G * N + G + G * L + 2 * L + 2 + XI;
+  const long T = G * N + G + G * L + L + 2 + XI;
+  const long A = 2 + 2 * L + G * L + G + G * N + XI;
   const long ncols = 2 + 2 * L + e->n_saved * (L + 1);
   const long nrows = e->cfg.iterations / e->cfg.thin;
   double* st = (double*)malloc(sizeof(double) * (size_t)S);
@@ -1118,6 +1222,7 @@ int orc_run_chain(const orc_engine* e, long chain, const cmc_output_view* out,
       for (long i = 0; i < G * L; ++i) orc_moments_update(&acc[k++], st[ST_BETA(e) + i]);
       for (long g = 0; g < G; ++g) orc_moments_update(&acc[k++], st[ST_GAMMA(e) + g]);
       for (long i = 0; i < G * N; ++i) orc_moments_update(&acc[k++], st[ST_EPS(e) + i]);
+      for (long i = 0; i < XI; ++i) orc_moments_update(&acc[k++], st[ST_XI(e) + i]);
       /* ContrastAccumulator::update, P:src/streaming.cpp:90-108 */
       ++ccount;
       const double mc = (double)ccount;

@@ -65,6 +65,8 @@ void orc_tau_fc_params(double a, double b, long G, double nu,
 void orc_theta_fc_params(double sum_beta, long G, double sigma, double c,
                          double* mean, double* sd);
 double orc_log_fc_sigma(double sigma, long G, double ss, double s_bound);
+/* extension (no reference): xi full conditional, CMC_PRIOR_* families */
+double orc_log_fc_xi(int prior, double xi, double q, double k);
 
 /* ---- slice (P:include/countmc/slice.hpp) ---- */
 typedef double (*orc_logf)(void* ctx, double x);

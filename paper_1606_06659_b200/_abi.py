@@ -54,7 +54,11 @@ class CmcProblem(ctypes.Structure):
     _fields_ = [("G", c_long), ("N", c_long), ("L", c_long),
                 ("counts", POINTER(c_longlong)), ("X", POINTER(c_double)),
                 ("h", POINTER(c_double)), ("a", c_double), ("b", c_double),
-                ("d", c_double), ("c", POINTER(c_double)), ("s", POINTER(c_double))]
+                ("d", c_double), ("c", POINTER(c_double)), ("s", POINTER(c_double)),
+                ("beta_prior", POINTER(c_int)), ("t_df", c_double)]
+
+
+PRIORS = {"normal": 0, "laplace": 1, "t": 2, "horseshoe": 3}
 
 
 class CmcRunConfig(ctypes.Structure):
@@ -111,7 +115,7 @@ def iptr(a: np.ndarray):
 class ProblemArrays:
     """Owns the numpy buffers a CmcProblem points into."""
 
-    def __init__(self, counts, X, h, a, b, d, c, s):
+    def __init__(self, counts, X, h, a, b, d, c, s, beta_prior=None, t_df=1.0):
         self.counts = np.ascontiguousarray(counts, dtype=np.int64)
         self.X = np.ascontiguousarray(X, dtype=np.float64)
         self.h = np.ascontiguousarray(h, dtype=np.float64)
@@ -119,10 +123,19 @@ class ProblemArrays:
         self.s = np.ascontiguousarray(s, dtype=np.float64)
         G, N = self.counts.shape
         L = self.X.shape[1]
+        self.prior = None
+        if beta_prior is not None and len(beta_prior):
+            codes = [PRIORS[x] if isinstance(x, str) else int(x) for x in beta_prior]
+            if len(codes) == 1 and L > 1:
+                codes = codes * L
+            self.prior = np.ascontiguousarray(codes, dtype=np.int32)
+        self.xi = self.prior is not None and bool((self.prior != 0).any())
         self.struct = CmcProblem(G, N, L,
                                  self.counts.ctypes.data_as(POINTER(c_longlong)),
                                  dptr(self.X), dptr(self.h), float(a), float(b),
-                                 float(d), dptr(self.c), dptr(self.s))
+                                 float(d), dptr(self.c), dptr(self.s),
+                                 self.prior.ctypes.data_as(POINTER(c_int))
+                                 if self.prior is not None else None, float(t_df))
 
 
 class ContrastArrays:
@@ -160,11 +173,13 @@ def make_config(chains=4, iterations=4000, burnin=2000, tune_cutoff=-1, thin=20,
                         sampler_mode, int(bool(concurrent_chains)))
 
 
-def sizes(G: int, N: int, L: int):
-    """(S, T, A): packed state, tuning and accumulator lengths."""
-    S = G * N + G + G * L + 2 * L + 2
-    T = G * N + G + G * L + L + 2
-    A = 2 + 2 * L + G * L + G + G * N
+def sizes(G: int, N: int, L: int, xi: bool = False):
+    """(S, T, A): packed state, tuning and accumulator lengths (xi: a ξ prior
+    on some column adds a trailing G x L block to each)."""
+    X = G * L if xi else 0
+    S = G * N + G + G * L + 2 * L + 2 + X
+    T = G * N + G + G * L + L + 2 + X
+    A = 2 + 2 * L + G * L + G + G * N + X
     return S, T, A
 
 

@@ -179,6 +179,10 @@ struct cmc_engine {
   std::vector<double> grp_val;
   int Jmax = 1;
   std::vector<long> saved;  // global, ascending
+  // xi-augmented beta priors (extension, no reference: parity unpinned)
+  std::vector<int> prior;  // L: CMC_PRIOR_*
+  bool xi_any = false;
+  double t_df = 1.0;
   // contrasts
   ContrastTable ctab{};
   bool has_ctab = false;
@@ -211,6 +215,7 @@ struct cmc_engine {
   DevBuf<double> eps, eps_w, eps_wa, gam, gam_w, gam_wa, beta, beta_w, beta_wa;
   DevBuf<double> log_gam, inv_gam, acc_eps, acc_gam, acc_beta, cprob, samples;
   DevBuf<double> partA, partB;
+  DevBuf<double> xi, xi_w, xi_wa, acc_xi;  // [C][L][G] (acc: [C][4][L][G])
   DevBuf<Hyper> hyper;
   DevBuf<ContrastTable> dctab;
   DevBuf<long> d_m;
@@ -270,7 +275,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaEventCreate(&e->ev0));
   CUDA_TRY(cudaEventCreate(&e->ev1));
   const long G = e->G, N = e->N, L = e->L, C = e->C;
-  const int Q = 2 + (int)L;
+  const int Q = 2 + (int)L + (e->xi_any ? (int)L : 0);
   // SoA y[n][g] as double (exact for counts < 2^53)
   std::vector<double> yh((size_t)N * G);
   for (long g = 0; g < G; ++g)
@@ -327,6 +332,12 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(e->acc_eps.alloc(4 * gn));
   CUDA_TRY(e->acc_gam.alloc(4 * gc));
   CUDA_TRY(e->acc_beta.alloc(4 * gl));
+  if (e->xi_any) {
+    CUDA_TRY(e->xi.alloc(gl));
+    CUDA_TRY(e->xi_w.alloc(gl));
+    CUDA_TRY(e->xi_wa.alloc(gl));
+    CUDA_TRY(e->acc_xi.alloc(4 * gl));
+  }
   CUDA_TRY(e->cprob.alloc(std::max<long>(1, prob_len(e)) * C));
   CUDA_TRY(e->samples.alloc(std::max<long>(1, e->n_cols * e->n_rows) * C));
   CUDA_TRY(e->hyper.alloc((size_t)C));
@@ -412,6 +423,13 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.partA = e->partA.p;
   p.partB = e->partB.p;
   p.C = (int)C;
+  p.xi_any = e->xi_any ? 1 : 0;
+  for (long l = 0; l < L; ++l) p.xi_fam[l] = e->prior[(size_t)l];
+  p.t_df = e->t_df;
+  p.xi = e->xi.p;
+  p.xi_w = e->xi_w.p;
+  p.xi_wa = e->xi_wa.p;
+  p.acc_xi = e->acc_xi.p;
   {
     int least = 0, greatest = 0;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -483,6 +501,7 @@ void initial_state_host(const cmc_engine* e, long chain, double* st) {
     nu = clamp_interior(nu + z(kSiteNu, 0), 1e-6 * e->d, (1.0 - 1e-6) * e->d);
     tau = std::max(1e-3, tau + z(kSiteTau, 0));
   }
+  if (e->xi_any) std::fill(sigma + L + 2, sigma + L + 2 + G * L, 1.0);  // xi block
 }
 
 // Upload one chain's packed state (+ optional tuning) into slot `c`.
@@ -507,6 +526,7 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
   CUDA_TRY(cudaMemcpy(e->gam.p + so * G, gam + g0, sizeof(double) * G,
                       cudaMemcpyHostToDevice));
   CUDA_TRY(put_gn(beta, e->beta.p + so * L * G, L));
+  if (e->xi_any) CUDA_TRY(put_gn(sigma + L + 2, e->xi.p + so * L * G, L));
   if (tw && ta) {
     const double* tws[2] = {tw, ta};
     double* de[2] = {e->eps_w.p, e->eps_wa.p};
@@ -518,6 +538,10 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
       CUDA_TRY(cudaMemcpy(dg[k] + so * G, t + Gt * N + g0, sizeof(double) * G,
                           cudaMemcpyHostToDevice));
       CUDA_TRY(put_gn(t + Gt * N + Gt, db[k] + so * L * G, L));
+      if (e->xi_any) {
+        double* dx = k == 0 ? e->xi_w.p : e->xi_wa.p;
+        CUDA_TRY(put_gn(t + Gt * N + Gt + Gt * L + L + 2, dx + so * L * G, L));
+      }
     }
   }
   Hyper hp;
@@ -579,6 +603,7 @@ int download_state(cmc_engine* e, long c, double* st, double* tw, double* ta,
     }
     sigma[L] = hp.nu;
     sigma[L + 1] = hp.tau;
+    if (e->xi_any) CUDA_TRY(get_gn(e->xi.p + so * L * G, sigma + L + 2, L));
   }
   double* tws[2] = {tw, ta};
   double* de[2] = {e->eps_w.p, e->eps_wa.p};
@@ -595,6 +620,9 @@ int download_state(cmc_engine* e, long c, double* st, double* tw, double* ta,
     for (long l = 0; l < L; ++l) t[off + l] = k == 0 ? hp.w_sigma[l] : hp.wa_sigma[l];
     t[off + L] = k == 0 ? hp.w_nu : hp.wa_nu;
     t[off + L + 1] = k == 0 ? hp.w_tau : hp.wa_tau;
+    if (e->xi_any)
+      CUDA_TRY(get_gn(k == 0 ? e->xi_w.p + so * L * G : e->xi_wa.p + so * L * G,
+                      t + off + L + 2, L));
   }
   return CMC_OK;
 }
@@ -624,11 +652,15 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
     if (step == 1 || step == 2 || step == 5) {
       // a stalled step leaves its value and width untouched on the device
       const size_t gl = (size_t)(g - e->g0), G = (size_t)e->G;
+      // step 5 with n == 1 is xi_gl (extension), drawn right after beta_gl
+      const bool xs5 = step == 5 && n == 1;
       const double* xs = step == 1 ? e->eps.p + (size_t)c * e->N * G + (size_t)n * G + gl
                          : step == 2 ? e->gam.p + (size_t)c * G + gl
+                         : xs5       ? e->xi.p + (size_t)c * e->L * G + (size_t)col * G + gl
                                      : e->beta.p + (size_t)c * e->L * G + (size_t)col * G + gl;
       const double* ws = step == 1 ? e->eps_w.p + (size_t)c * e->N * G + (size_t)n * G + gl
                          : step == 2 ? e->gam_w.p + (size_t)c * G + gl
+                         : xs5       ? e->xi_w.p + (size_t)c * e->L * G + (size_t)col * G + gl
                                      : e->beta_w.p + (size_t)c * e->L * G + (size_t)col * G + gl;
       CUDA_TRY(cudaMemcpy(&x0, xs, sizeof(double), cudaMemcpyDeviceToHost));
       CUDA_TRY(cudaMemcpy(&w, ws, sizeof(double), cudaMemcpyDeviceToHost));
@@ -643,7 +675,7 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
       case 2: set_stall(err, "gamma", g + 1, -1, x0, w, it); break;
       case 3: set_stall(err, "nu", -1, -1, x0, w, it); break;
       case 4: set_stall(err, "tau", -1, -1, x0, w, it); break;
-      case 5: set_stall(err, "beta", g + 1, col + 1, x0, w, it); break;
+      case 5: set_stall(err, n == 1 ? "xi" : "beta", g + 1, col + 1, x0, w, it); break;
       default: set_stall(err, "sigma", col + 1, -1, x0, w, it); break;
     }
     return CMC_ERR_STALL;
@@ -670,7 +702,7 @@ cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p, int chains,
     if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
   } else {
-    const int Q = 2 + (int)e->L;
+    const int Q = 2 + (int)e->L + (e->xi_any ? (int)e->L : 0);
     const size_t cA = (size_t)e->C * Q * p.leaves_per_rank;
     const size_t cB = (size_t)e->C * e->L * p.leaves_per_rank;
     if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
@@ -804,6 +836,13 @@ int cmc_engine_create(const cmc_problem* p, const cmc_run_config* config,
   for (long l = 0; l < p->L; ++l)
     if (!(p->c[l] > 0.0) || !(p->s[l] > 0.0))
       return fail_config(err, "prior entries c, s must be strictly positive");
+  if (p->beta_prior)
+    for (long l = 0; l < p->L; ++l) {
+      if (p->beta_prior[l] < CMC_PRIOR_NORMAL || p->beta_prior[l] > CMC_PRIOR_HORSESHOE)
+        return fail_config(err, "beta prior must be normal, laplace, t or horseshoe");
+      if (p->beta_prior[l] == CMC_PRIOR_T && !(p->t_df > 0.0))
+        return fail_config(err, "t prior needs positive degrees of freedom");
+    }
   // device limits of this build
   if (p->L > kLMax) return fail_config(err, "L exceeds the 16 columns this build supports");
   if (p->N >= (1 << 20)) return fail_config(err, "N too large for this build");
@@ -835,6 +874,10 @@ int cmc_engine_create(const cmc_problem* p, const cmc_run_config* config,
   e->a = p->a;
   e->b = p->b;
   e->d = p->d;
+  e->prior.assign((size_t)p->L, CMC_PRIOR_NORMAL);
+  if (p->beta_prior) e->prior.assign(p->beta_prior, p->beta_prior + p->L);
+  for (int v : e->prior) e->xi_any |= v != CMC_PRIOR_NORMAL;
+  e->t_df = p->t_df;
   e->cfg = cfg;
   e->device = device;
   e->C = (int)cfg.chains;
@@ -966,7 +1009,7 @@ int cmc_engine_destroy(cmc_engine* e) {
                             &e->gam_wa, &e->beta, &e->beta_w, &e->beta_wa,
                             &e->log_gam, &e->inv_gam, &e->acc_eps, &e->acc_gam,
                             &e->acc_beta, &e->cprob, &e->samples, &e->partA,
-                            &e->partB};
+                            &e->partB, &e->xi, &e->xi_w, &e->xi_wa, &e->acc_xi};
     for (auto* b : ds) b->free_();
     e->goff.free_();
     e->gmoff.free_();
@@ -1102,8 +1145,9 @@ int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
-  const long S = e->G_total * e->N + e->G_total + e->G_total * e->L + 2 * e->L + 2;
-  const long T = e->G_total * e->N + e->G_total + e->G_total * e->L + e->L + 2;
+  const long XI = e->xi_any ? e->G_total * e->L : 0;
+  const long S = e->G_total * e->N + e->G_total + e->G_total * e->L + 2 * e->L + 2 + XI;
+  const long T = e->G_total * e->N + e->G_total + e->G_total * e->L + e->L + 2 + XI;
   std::vector<double> st((size_t)S), tw((size_t)T, e->cfg.w_init), ta((size_t)T, 0.0);
   CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * e->C));
   for (long c = 0; c < e->C; ++c) {
@@ -1113,6 +1157,7 @@ int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaMemset(e->acc_eps.p, 0, sizeof(double) * e->acc_eps.n));
   CUDA_TRY(cudaMemset(e->acc_gam.p, 0, sizeof(double) * e->acc_gam.n));
   CUDA_TRY(cudaMemset(e->acc_beta.p, 0, sizeof(double) * e->acc_beta.n));
+  if (e->xi_any) CUDA_TRY(cudaMemset(e->acc_xi.p, 0, sizeof(double) * e->acc_xi.n));
   CUDA_TRY(cudaMemset(e->cprob.p, 0, sizeof(double) * e->cprob.n));
   CUDA_TRY(cudaMemset(e->samples.p, 0, sizeof(double) * e->samples.n));
   long one = 1;
@@ -1560,6 +1605,23 @@ int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,
       for (long g = a; g < b; ++g)
         for (long n = 0; n < N; ++n) dst[i + (g0 + g) * N + n] = buf[(size_t)n * G + g];
     });
+    i += Gt * N;
+    if (e->xi_any) {
+      // xi block (extension): sampled columns from the device; a normal
+      // column's xi is the constant 1, whose compensated Welford state after
+      // `count` updates is (1, 1, 0, 0)
+      buf.resize((size_t)L * G);
+      CUDA_TRY(cudaMemcpy(buf.data(), e->acc_xi.p + so * 4 * L * G + (size_t)k * L * G,
+                          sizeof(double) * L * G, cudaMemcpyDeviceToHost));
+      const double konst = (k < 2 && count > 0) ? 1.0 : 0.0;
+      host_parallel_for(G, [&](long a, long b) {
+        for (long g = a; g < b; ++g)
+          for (long l = 0; l < L; ++l)
+            dst[i + (g0 + g) * L + l] = e->prior[(size_t)l] != CMC_PRIOR_NORMAL
+                                            ? buf[(size_t)l * G + g]
+                                            : konst;
+      });
+    }
   }
   if (e->has_ctab) {
     if (o->contrast_prob)

@@ -35,6 +35,7 @@ enum : uint64_t {
   kSiteSigma = 7,
   kSiteSaveSel = 8,
   kSiteSim = 9,
+  kSiteXi = 11,  // extension: xi priors (10 is the reference's resample)
 };
 CMC_HD uint64_t site_id(uint64_t family, uint64_t flat) {
   return (family << 56) | flat;

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/countmc_b200.h"
+
 namespace cmc {
 
 constexpr int kLMax = 16;         // model-matrix columns supported
@@ -115,7 +117,7 @@ struct SweepParams {
   double* samples;  // [C][n_cols][n_rows]
   const int* saved_slot;  // [G] local: saved index or -1
   // reductions
-  double* partA;  // [world][C][2+L][leaves_per_rank]
+  double* partA;  // [world][C][Q][leaves_per_rank], Q = leaf_q_a(L, xi_any)
   double* partB;  // [world][C][L][leaves_per_rank]
   int C;          // chains resident (stride of the partial buffers)
   // optional block timeline (debug/profiling): per record {kernel<<56 |
@@ -126,7 +128,19 @@ struct SweepParams {
   // launch priorities (host side): the tail and gene kernels are on the
   // critical path, the next sweep's eps kernel is not
   int prio_eps, prio_gene, prio_tail;
+  // xi-augmented beta priors (extension, no reference: parity unpinned).
+  // With xi_any the leaf buffer partA carries 2 + 2L quantities: [log gamma,
+  // 1/gamma, S_l, W_l] with S_l = sum beta_l (normal column) or sum
+  // beta_l/xi_l, and W_l = sum 1/xi_l; partB holds sum (beta-theta)^2[/xi].
+  int xi_any;
+  int xi_fam[kLMax];  // CMC_PRIOR_* per column
+  double t_df;
+  double *xi, *xi_w, *xi_wa;  // [C][L][G]
+  double* acc_xi;             // [C][4][L][G]
 };
+
+// leaf quantities of partA
+__host__ __device__ inline int leaf_q_a(int L, int xi_any) { return 2 + L + (xi_any ? L : 0); }
 
 // Launch wrappers (sweep_kernels.cu).  `chains` = grid.y.
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,

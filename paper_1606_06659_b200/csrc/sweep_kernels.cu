@@ -281,6 +281,22 @@ struct BetaF {
   }
 };
 
+// xi full conditional (extension, no reference: parity unpinned), the
+// oracle's orc_log_fc_xi: q = (beta - theta)^2 / (2 sigma^2),
+//   laplace   -log(x)/2 - q/x - x/2
+//   t(k)      -(k/2 + 3/2) log(x) - (q + k/2)/x
+//   horseshoe -log(x) - q/x - log1p(x)
+struct XiF {
+  int fam;
+  double q, k;
+  __device__ __forceinline__ double operator()(double x) const {
+    if (!(x > 0.0)) return -INFINITY;
+    if (fam == CMC_PRIOR_LAPLACE) return -0.5 * log(x) - q / x - 0.5 * x;
+    if (fam == CMC_PRIOR_T) return -(0.5 * k + 1.5) * log(x) - (q + 0.5 * k) / x;
+    return -log(x) - q / x - log1p(x);
+  }
+};
+
 // BetaF with the (at most JR) group sums in registers: same terms in the
 // same order; each term is branch-free (the clamp and S_j = 0 cases select
 // their value), which keeps the slice loop's evaluation straight-line.
@@ -509,7 +525,9 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 #endif
 // JR > 0: every column has at most JR groups, kept in registers
 // (BetaFR); JR = 0: any design, group sums in shared memory (BetaF).
-template <int JR>
+// XI: some column has a xi prior (extension); the reference model (all
+// normal) is compiled without the xi step.
+template <int JR, bool XI>
 __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
     gene_sweep_kernel(const SweepParams p, const long m_off) {
   extern __shared__ double smem[];
@@ -606,6 +624,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
   for (int l = 0; l < L; ++l) {
     const size_t i = (size_t)l * G + gl;
     const int jb = __ldg(p.grp_off + l), je = __ldg(p.grp_off + l + 1);
+    const bool xcol = XI && p.xi_fam[l] != CMC_PRIOR_NORMAL;  // warp-uniform
     double bold = 0.0, bnew = 0.0, w0 = 0.0, w = 0.0, wa = 0.0;
     bool st = false;
     __syncwarp();
@@ -631,6 +650,9 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
       };
       const double sig = hp->sigma[l];
       const double sig2 = sig * sig;
+      // prior variance sigma_l^2 (normal) or sigma_l^2 xi_gl (xi column)
+      const double inv2v = xcol ? 1.0 / (2.0 * (sig2 * p.xi[so * L * G + i]))
+                                : 1.0 / (2.0 * sig2);
       w0 = beta_w[i];
       w = w0;
       wa = tuning ? beta_wa[i] : 0.0;
@@ -640,7 +662,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
         BetaFR<JR> f;
         f.a = __ldg(p.A + i);
         f.theta = hp->theta[l];
-        f.inv_two_sig2 = 1.0 / (2.0 * sig2);
+        f.inv_two_sig2 = inv2v;
         f.e700 = p.exp_clamp;
         f.tab = etab;
         f.J = je - jb;
@@ -664,34 +686,77 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
           sS[(j - jb) * kGeneBlock + tid] = s;
           sLogS[(j - jb) * kGeneBlock + tid] = log(s);
         }
-        BetaF f{__ldg(p.A + i), hp->theta[l], 1.0 / (2.0 * sig2), p.exp_clamp,
+        BetaF f{__ldg(p.A + i), hp->theta[l], inv2v, p.exp_clamp,
                 p.grp_val + jb, sS + tid, sLogS + tid, etab, je - jb, 0u};
         bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
         clamps += f.clamps;
       }
     }
     __syncwarp();
-    if (!alive) continue;
-    if (st) {
-      record_stall(hp, stall_key(5, l, gg, 0), m);
-      alive = false;
-      continue;
-    }
-    beta[i] = bnew;
-    if (tuning) {
-      beta_w[i] = w;
-      beta_wa[i] = wa;
-    }
-    if (bnew != bold) {
-      for (int j = jb; j < je; ++j) {
-        const double v = __ldg(p.grp_val + j);
-        for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
-          const int n = __ldg(p.grp_mem + q);
-          xs[n * kGeneBlock + tid] += v * (bnew - bold);
+    auto commit_beta = [&]() {
+      beta[i] = bnew;
+      if (tuning) {
+        beta_w[i] = w;
+        beta_wa[i] = wa;
+      }
+      if (bnew != bold) {
+        for (int j = jb; j < je; ++j) {
+          const double v = __ldg(p.grp_val + j);
+          for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
+            const int n = __ldg(p.grp_mem + q);
+            xs[n * kGeneBlock + tid] += v * (bnew - bold);
+          }
         }
       }
+      if (monitor) moments(p.acc_beta + so * 4 * L * G + i, (size_t)L * G, bnew, mcount);
+    };
+    if constexpr (!XI) {
+      if (!alive) continue;
+      if (st) {
+        record_stall(hp, stall_key(5, l, gg, 0), m);
+        alive = false;
+        continue;
+      }
+      commit_beta();
+      continue;
     }
-    if (monitor) moments(p.acc_beta + so * 4 * L * G + i, (size_t)L * G, bnew, mcount);
+    // xi engines: every lane passes the same __syncwarp sequence
+    if (alive && st) {
+      record_stall(hp, stall_key(5, l, gg, 0), m);
+      alive = false;
+    }
+    if (alive) commit_beta();
+    if (xcol) {
+      // xi_gl right after beta_gl (extension; reads beta_gl, theta_l and
+      // sigma_l of iteration m-1, like the oracle's step 5)
+      double xnew = 0.0, xw = 0.0, xwa = 0.0;
+      bool xst = false;
+      const size_t ix = so * L * G + i;
+      __syncwarp();
+      if (alive) {
+        const double sg = hp->sigma[l];
+        const double dz = bnew - hp->theta[l];
+        XiF f{p.xi_fam[l], dz * dz / (2.0 * (sg * sg)), p.t_df};
+        xw = p.xi_w[ix];
+        xwa = tuning ? p.xi_wa[ix] : 0.0;
+        Stream rng;
+        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteXi, gg * L + l));
+        xnew = slice_step(f, p.xi[ix], xw, xwa, sc, m, rng, xst);
+      }
+      __syncwarp();
+      if (alive && xst) {
+        record_stall(hp, stall_key(5, l, gg, 1), m);
+        alive = false;
+      }
+      if (alive) {
+        p.xi[ix] = xnew;
+        if (tuning) {
+          p.xi_w[ix] = xw;
+          p.xi_wa[ix] = xwa;
+        }
+        if (monitor) moments(p.acc_xi + so * 4 * L * G + i, (size_t)L * G, xnew, mcount);
+      }
+    }
   }
 
   __syncwarp();
@@ -803,17 +868,26 @@ __device__ double warp_pairwise_leaves(const double* part, const SweepParams& p,
 
 // Steps 3, 4 and 6: nu, tau and theta from the gathered leaf sums.  Called
 // by a whole block of 32*(2+L) threads (warp q reduces quantity q).
+template <bool XI>
 __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
-  __shared__ double red[2 + kLMax];
+  __shared__ double red[XI ? 2 + 2 * kLMax : 2 + kLMax];
   Hyper* hp = p.hyper + slot;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint64_t chain = (uint64_t)(p.chain_base + (slot - p.slot_base));
-  const int L = p.L, Q = 2 + L;
+  const int L = p.L, Q = leaf_q_a(L, p.xi_any);
   const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   const double Gd = (double)p.G_total;
-  if (warp < Q) {
-    const double r = warp_pairwise_leaves(p.partA, p, slot, Q, warp, p.n_leaves_total);
-    if ((tid & 31) == 0) red[warp] = r;
+  if constexpr (!XI) {
+    (void)nwarps;
+    if (warp < Q) {
+      const double r = warp_pairwise_leaves(p.partA, p, slot, Q, warp, p.n_leaves_total);
+      if ((tid & 31) == 0) red[warp] = r;
+    }
+  } else {  // Q = 2 + 2L may exceed the block's 32 warps
+    for (int q = warp; q < Q; q += nwarps) {
+      const double r = warp_pairwise_leaves(p.partA, p, slot, Q, q, p.n_leaves_total);
+      if ((tid & 31) == 0) red[q] = r;
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -868,7 +942,10 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
     const int l = tid - 32;
     const double sb = red[2 + l];
     const double sg = hp->sigma[l], c = p.c[l];
-    const double v = 1.0 / (1.0 / (c * c) + Gd / (sg * sg));
+    // xi column (extension): precision 1/c^2 + sum_g 1/(sigma^2 xi_g), with
+    // sb = sum_g beta_g / xi_g (the oracle's step 6)
+    const double gw = (XI && p.xi_fam[l] != CMC_PRIOR_NORMAL) ? red[2 + L + l] : Gd;
+    const double v = 1.0 / (1.0 / (c * c) + gw / (sg * sg));
     const double mean = v * sb / (sg * sg);
     const double sd = sqrt(v);
     Stream rng;
@@ -966,37 +1043,61 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned total
 
 // Leaf sums of log gamma (q=0), 1/gamma (q=1), beta_l (q=2+l); one warp
 // per quantity, one block per local leaf.
+template <bool XI>
 __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
   WarpTrace wt(p, 3, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
   if (stalled_chain(hp)) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int L = p.L, Q = 2 + L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int L = p.L, Q = leaf_q_a(L, p.xi_any);
   const size_t G = (size_t)p.G, so = (size_t)slot;
   const long lb = blockIdx.x;
   const long start = lb * kLeaf;
   const long end = min((long)G, start + kLeaf);
-  if (warp < Q) {
-    const double* src = warp == 0   ? p.log_gam + so * G
-                        : warp == 1 ? p.inv_gam + so * G
-                                    : p.beta + so * L * G + (size_t)(warp - 2) * G;
-    const double s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
-    if (lane == 0) {
-      const long lpr = p.leaves_per_rank;
-      const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
-      p.partA[((rank * p.C + slot) * Q + warp) * lpr + lb] = s;
+  const long lpr = p.leaves_per_rank;
+  const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
+  if constexpr (!XI) {
+    if (warp < Q) {
+      const double* src = warp == 0   ? p.log_gam + so * G
+                          : warp == 1 ? p.inv_gam + so * G
+                                      : p.beta + so * L * G + (size_t)(warp - 2) * G;
+      const double s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
+      if (lane == 0) p.partA[((rank * p.C + slot) * Q + warp) * lpr + lb] = s;
+    }
+  } else {
+    // xi engine: quantities [log gamma, 1/gamma, S_l, W_l] (sweep.h), looped
+    // when Q exceeds the 32 warps of a block
+    for (int q = warp; q < Q; q += nwarps) {
+      double s;
+      if (q < 2) {
+        const double* src = q == 0 ? p.log_gam + so * G : p.inv_gam + so * G;
+        s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
+      } else if (q < 2 + L) {
+        const double* src = p.beta + so * L * G + (size_t)(q - 2) * G;
+        if (p.xi_fam[q - 2] != CMC_PRIOR_NORMAL) {
+          const double* xs = p.xi + so * L * G + (size_t)(q - 2) * G;
+          s = warp_leaf_sum([&](long i) { return src[i] / xs[i]; }, start, end);
+        } else {
+          s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
+        }
+      } else {
+        const double* xs = p.xi + so * L * G + (size_t)(q - 2 - L) * G;
+        s = warp_leaf_sum([&](long i) { return 1.0 / xs[i]; }, start, end);
+      }
+      if (lane == 0) p.partA[((rank * p.C + slot) * Q + q) * lpr + lb] = s;
     }
   }
   if (!p.fuse_tail) return;
   if (!last_block(&hp->doneA, (unsigned)p.n_leaves_local)) return;
-  hyper_a_body(p, slot, *p.d_m + m_off);
+  hyper_a_body<XI>(p, slot, *p.d_m + m_off);
 }
 
+template <bool XI>
 __global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
   const int slot = p.slot_base + blockIdx.x;
   if (stalled_chain(p.hyper + slot)) return;
-  hyper_a_body(p, slot, *p.d_m + m_off);
+  hyper_a_body<XI>(p, slot, *p.d_m + m_off);
 }
 
 // Leaf sums of (beta_l - theta_l)^2 with theta of this iteration.
@@ -1014,12 +1115,23 @@ __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
   if (warp < L) {
     const double th = hp->theta[warp];
     const double* src = p.beta + so * L * G + (size_t)warp * G;
-    const double s = warp_leaf_sum(
-        [&](long i) {
-          const double dl = src[i] - th;
-          return dl * dl;
-        },
-        start, end);
+    double s;
+    if (p.xi_any && p.xi_fam[warp] != CMC_PRIOR_NORMAL) {  // extension: /xi
+      const double* xs = p.xi + so * L * G + (size_t)warp * G;
+      s = warp_leaf_sum(
+          [&](long i) {
+            const double dl = src[i] - th;
+            return dl * dl / xs[i];
+          },
+          start, end);
+    } else {
+      s = warp_leaf_sum(
+          [&](long i) {
+            const double dl = src[i] - th;
+            return dl * dl;
+          },
+          start, end);
+    }
     if (lane == 0) {
       const long lpr = p.leaves_per_rank;
       const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
@@ -1102,39 +1214,52 @@ cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
   return launch_prio(eps_sweep_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_eps, p, m_off);
 }
 
-template <int JR>
+template <int JR, bool XI>
 static cudaError_t launch_gene_sweep_t(const SweepParams& p, int chains, long m_off,
                                        cudaStream_t s) {
   const int smem = gene_sweep_smem_bytes(p.N, JR > 0 ? 0 : p.Jmax);
   static int configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(
-        gene_sweep_kernel<JR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        gene_sweep_kernel<JR, XI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)chains);
-  return launch_prio(gene_sweep_kernel<JR>, grid, dim3(kGeneBlock), smem, s, p.prio_gene, p,
+  return launch_prio(gene_sweep_kernel<JR, XI>, grid, dim3(kGeneBlock), smem, s, p.prio_gene, p,
                      m_off);
 }
 
 cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
                               cudaStream_t s) {
-  if (p.Jmax <= 2) return launch_gene_sweep_t<2>(p, chains, m_off, s);
-  return launch_gene_sweep_t<0>(p, chains, m_off, s);
+  if (p.xi_any) {
+    if (p.Jmax <= 2) return launch_gene_sweep_t<2, true>(p, chains, m_off, s);
+    return launch_gene_sweep_t<0, true>(p, chains, m_off, s);
+  }
+  if (p.Jmax <= 2) return launch_gene_sweep_t<2, false>(p, chains, m_off, s);
+  return launch_gene_sweep_t<0, false>(p, chains, m_off, s);
 }
 
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
                           cudaStream_t s) {
-  const int Q = 2 + p.L;
-  const int threads = 32 * (Q > 2 ? Q : 2);
+  const int Q = leaf_q_a(p.L, p.xi_any);
+  const int threads = 32 * (Q < 32 ? Q : 32);
   dim3 grid((unsigned)p.n_leaves_local, (unsigned)chains);
-  return launch_prio(leaf_a_kernel, grid, dim3(threads < 64 ? 64 : threads), 0, s, p.prio_tail, p, m_off);
+  if (p.xi_any)
+    return launch_prio(leaf_a_kernel<true>, grid, dim3(threads < 64 ? 64 : threads), 0, s,
+                       p.prio_tail, p, m_off);
+  return launch_prio(leaf_a_kernel<false>, grid, dim3(threads < 64 ? 64 : threads), 0, s,
+                     p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_hyper_a(const SweepParams& p, int chains, long m_off,
                            cudaStream_t s) {
-  return launch_prio(hyper_a_kernel, dim3(chains), dim3(32 * (2 + p.L)), 0, s, p.prio_tail, p, m_off);
+  const int Q = leaf_q_a(p.L, p.xi_any);
+  if (p.xi_any)
+    return launch_prio(hyper_a_kernel<true>, dim3(chains), dim3(32 * (Q < 32 ? Q : 32)), 0, s,
+                       p.prio_tail, p, m_off);
+  return launch_prio(hyper_a_kernel<false>, dim3(chains), dim3(32 * (Q < 32 ? Q : 32)), 0, s,
+                     p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_leaf_b(const SweepParams& p, int chains, long m_off,

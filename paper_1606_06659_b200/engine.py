@@ -113,6 +113,12 @@ class PriorConfig:
     d: float = 1000.0
     c: Optional[Sequence[float]] = None  # prior sd of theta_l, default 10
     s: Optional[Sequence[float]] = None  # upper bound of sigma_l, default 100
+    # Extension (not in the reference; parity unpinned): per
+    # column "normal" (the reference model), "laplace", "t" or "horseshoe"
+    # -- beta_gl ~ N(theta_l, sigma_l^2 xi_gl) with xi_gl from that prior.
+    # One entry applies to every column; t_df is k of the t prior.
+    beta_prior: Sequence[str] = ()
+    t_df: float = 1.0
 
     def resolve(self, L: int):
         """PriorConfig::resolve, P:src/types.cpp:38-43."""
@@ -160,10 +166,12 @@ class CountMatrix:
 
 
 class ChainState:
-    """One iteration's parameter values (reference ChainState)."""
+    """One iteration's parameter values (reference ChainState).  ``xi``
+    (G x L) exists only with a xi prior (extension)."""
 
-    def __init__(self, G, N, L):
+    def __init__(self, G, N, L, xi=False):
         self.G, self.N, self.L = G, N, L
+        self.xi = np.ones((G, L)) if xi else None
         self.eps = np.zeros((G, N))
         self.gamma = np.ones(G)
         self.beta = np.zeros((G, L))
@@ -173,12 +181,15 @@ class ChainState:
         self.tau = 1.0
 
     def pack(self) -> np.ndarray:
-        return np.concatenate([self.eps.ravel(), self.gamma, self.beta.ravel(),
-                               self.theta, self.sigma, [self.nu, self.tau]]).astype(np.float64)
+        parts = [self.eps.ravel(), self.gamma, self.beta.ravel(), self.theta, self.sigma,
+                 [self.nu, self.tau]]
+        if self.xi is not None:
+            parts.append(self.xi.ravel())
+        return np.concatenate(parts).astype(np.float64)
 
     @classmethod
     def unpack(cls, packed, G, N, L) -> "ChainState":
-        st = cls(G, N, L)
+        st = cls(G, N, L, xi=len(packed) > sizes(G, N, L)[0])
         st.load(packed)
         return st
 
@@ -190,7 +201,9 @@ class ChainState:
         self.beta = np.array(p[o:o + G * L]).reshape(G, L); o += G * L
         self.theta = np.array(p[o:o + L]); o += L
         self.sigma = np.array(p[o:o + L]); o += L
-        self.nu = float(p[o]); self.tau = float(p[o + 1])
+        self.nu = float(p[o]); self.tau = float(p[o + 1]); o += 2
+        if len(p) > o:
+            self.xi = np.array(p[o:o + G * L]).reshape(G, L)
 
     def check(self, priors: PriorConfig):
         """ChainState::check, P:src/types.cpp:71-89."""
@@ -213,10 +226,11 @@ class ChainState:
 
 
 class TuningState:
-    """Slice widths w and w_aux in the packed order [eps|gamma|beta|sigma|nu|tau]."""
+    """Slice widths w and w_aux in the packed order
+    [eps|gamma|beta|sigma|nu|tau] (+ [xi] with a xi prior)."""
 
-    def __init__(self, G, N, L, w_init=1.0):
-        _, T, _ = sizes(G, N, L)
+    def __init__(self, G, N, L, w_init=1.0, xi=False):
+        _, T, _ = sizes(G, N, L, xi)
         self.G, self.N, self.L = G, N, L
         self.w = np.full(T, float(w_init))
         self.w_aux = np.zeros(T)
@@ -225,7 +239,8 @@ class TuningState:
         G, N, L = self.G, self.N, self.L
         o = {"eps": (0, G * N), "gamma": (G * N, G), "beta": (G * N + G, G * L),
              "sigma": (G * N + G + G * L, L), "nu": (G * N + G + G * L + L, 1),
-             "tau": (G * N + G + G * L + L + 1, 1)}[which]
+             "tau": (G * N + G + G * L + L + 1, 1),
+             "xi": (G * N + G + G * L + L + 2, G * L)}[which]
         return slice(o[0], o[0] + o[1])
 
     def width(self, which):
@@ -287,6 +302,7 @@ class ChainOutput:
     step_seconds: np.ndarray
     clamp_events: int
     final_state: ChainState
+    xi_acc: Optional[Moments] = None  # G x L, with a xi prior (extension)
 
 
 # ----------------------------------------------------------------- contrasts
@@ -380,7 +396,8 @@ class GibbsEngine:
         self._genes = list(data.genes) if isinstance(data, CountMatrix) and data.genes else None
         self._prob = ProblemArrays(counts, spec.X, spec.h, spec.priors.a,
                                    spec.priors.b, spec.priors.d, spec.priors.c,
-                                   spec.priors.s)
+                                   spec.priors.s, spec.priors.beta_prior, spec.priors.t_df)
+        self.xi = self._prob.xi
         self._ctr = ContrastArrays([c.flat() for c in self._contrast_specs])
         cfg_c = cfg.to_c()
         err = CmcError()
@@ -449,7 +466,7 @@ class GibbsEngine:
         return self._h
 
     def initial_state(self, chain: int) -> ChainState:
-        S, _, _ = sizes(self.G, self.N, self.L)
+        S, _, _ = sizes(self.G, self.N, self.L, self.xi)
         buf = np.zeros(S)
         err = CmcError()
         _raise(self._lib.cmc_engine_initial_state(self._h, chain, dptr(buf), byref(err)), err)
@@ -569,9 +586,13 @@ class GibbsEngine:
             names += [f"beta[{g + 1},{l + 1}]" for l in range(L)] + [f"gamma[{g + 1}]"]
         return names
 
+    def tuning_state(self) -> TuningState:
+        """A TuningState of this engine's layout at w_init."""
+        return TuningState(self.G, self.N, self.L, self._cfg.slice.w_init, self.xi)
+
     def _output(self, chain: int) -> ChainOutput:
         G, N, L = self.G, self.N, self.L
-        S, _, A = sizes(G, N, L)
+        S, _, A = sizes(G, N, L, self.xi)
         accs = [np.zeros(A) for _ in range(4)]
         count = np.zeros(1, dtype=np.int64)
         n_prob = sum(G if c.per_gene else 1 for c in self._contrast_specs)
@@ -601,7 +622,8 @@ class GibbsEngine:
         sigma = part(o, L); o += L
         beta = part(o, G * L, (G, L)); o += G * L
         gamma = part(o, G); o += G
-        eps = part(o, G * N, (G, N))
+        eps = part(o, G * N, (G, N)); o += G * N
+        xi = part(o, G * L, (G, L)) if self.xi else None
         contrasts, off = [], 0
         for k, c in enumerate(self._contrast_specs):
             n = G if c.per_gene else 1
@@ -610,7 +632,7 @@ class GibbsEngine:
         return ChainOutput(chain, nu, tau, theta, sigma, beta, gamma, eps, contrasts,
                            self.sample_names(), samples[:self.n_cols * rows].reshape(self.n_cols, rows),
                            iters[:rows], self._saved.copy(), secs, int(clamps[0]),
-                           ChainState.unpack(final, G, N, L))
+                           ChainState.unpack(final, G, N, L), xi)
 
 
 # ---------------------------------------------------------- synthetic inputs

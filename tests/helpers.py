@@ -56,7 +56,9 @@ class Product:
         self.cfg = cfg
         self.prob = ProblemArrays(counts, X, h, pr.get("a", 1.0), pr.get("b", 1.0),
                                   pr.get("d", 1000.0), pr.get("c", [10.0] * L),
-                                  pr.get("s", [100.0] * L))
+                                  pr.get("s", [100.0] * L), pr.get("beta_prior"),
+                                  pr.get("t_df", 1.0))
+        self.xi = self.prob.xi
         self.contrasts = list(contrasts)
         self.ctr = ContrastArrays(self.contrasts)
         err = CmcError()
@@ -73,7 +75,7 @@ class Product:
             self.lib.cmc_engine_destroy(self.h)
 
     def initial_state(self, chain):
-        S, _, _ = sizes(self.G, self.N, self.L)
+        S, _, _ = sizes(self.G, self.N, self.L, self.xi)
         st = np.zeros(S)
         err = CmcError()
         assert self.lib.cmc_engine_initial_state(self.h, chain, dptr(st), byref(err)) == 0
@@ -115,7 +117,7 @@ class Product:
         outs = []
         for c in range(self.cfg.chains):
             o, view = oracle.new_outputs(self.G, self.N, self.L, n_saved, n_rows, n_prob,
-                                         len(self.contrasts))
+                                         len(self.contrasts), self.xi)
             rc = self.lib.cmc_engine_get_output(self.h, c, byref(view), byref(err))
             assert rc == 0, err.msg
             outs.append(o)
@@ -125,7 +127,7 @@ class Product:
 def packed_start(engine_like, chain, w_init=1.0):
     st = engine_like.initial_state(chain)
     G, N, L = engine_like.G, engine_like.N, engine_like.L
-    _, T, _ = sizes(G, N, L)
+    _, T, _ = sizes(G, N, L, getattr(engine_like, "xi", False))
     return st, np.full(T, w_init), np.zeros(T)
 
 
