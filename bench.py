@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--e2e-iterations", type=int, default=4000)  # reference RunConfig default
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-xi", action="store_true")
     return ap.parse_args()
 
 
@@ -289,6 +290,39 @@ def run_b200(a, rank, world, local_rank):
     del eng
     torch.cuda.synchronize()
 
+    # BASELINE configs[1] names Laplace priors, configs[2] t and horseshoe:
+    # the xi extension (not in the reference; parity unpinned)
+    # timed the same way on the same data.  The headline stays the normal
+    # prior, the only model the reference (and so the reference arm) has.
+    xi_rates = None
+    if not dist and not a.no_xi:
+        xi_rates = {}
+        from paper_1606_06659_b200 import PriorConfig
+        for name in ("laplace", "t", "horseshoe"):
+            spec = ModelSpec(X, h, PriorConfig(beta_prior=[name], t_df=3.0))
+            ex = GibbsEngine(CountMatrix(counts), spec,
+                             RunConfig(chains=C, burnin=B, iterations=W + K, thin=20, seed=7,
+                                       save_genes=20),
+                             contrasts=[heterosis_contrast()], device=local_rank)
+            lx, hx = ex._lib, ex.handle
+            ok(lx.cmc_engine_begin(hx, byref(err)))
+            ok(lx.cmc_engine_sweeps(hx, 1, B + 1 + W, byref(err)))
+            ok(lx.cmc_engine_sync(hx, byref(err)))
+            sx = torch.cuda.ExternalStream(lx.cmc_engine_stream(hx))
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            x0.record(sx)
+            ok(lx.cmc_engine_sweeps(hx, B + 1 + W, B + 1 + W + K, byref(err)))
+            x1.record(sx)
+            ok(lx.cmc_engine_sync(hx, byref(err)))
+            torch.cuda.synchronize()
+            xms = x0.elapsed_time(x1)
+            xi_rates[name] = {"value": C * G * K / (xms * 1e-3), "ms_per_step": xms / K}
+            del ex
+        xi_rates["note"] = ("beta_gl ~ N(theta_l, sigma_l^2 xi_gl) with a xi slice step per "
+                            "(gene, column); t with k = 3; same data, chains, burn-in and "
+                            "device timing as value; extension, not in the reference")
+
     # end to end through the public API from host arrays: create (H2D of
     # counts + initial states), run() (burn-in + iterations), all outputs D2H
     E, BE = a.e2e_iterations, a.e2e_burnin
@@ -361,6 +395,7 @@ def run_b200(a, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clk,
         "burnin": burnin,
+        "xi_priors": xi_rates,
         "e2e": e2e,
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -149,6 +149,10 @@ struct Problem {
   std::vector<double> X, h;
   double a = 1.0, b = 1.0, d = 1000.0;
   std::vector<double> c, s;  // empty -> reference defaults 10 and 100
+  // extension (not in the reference): per-column CMC_PRIOR_* xi priors
+  // (empty = the reference's normal prior) and the t prior's k
+  std::vector<int> beta_prior;
+  double t_df = 1.0;
 };
 
 // ChainState (P:include/countmc/types.hpp:86-108) in packed form.
@@ -168,8 +172,10 @@ struct ChainState {
 struct TuningState {
   std::vector<double> w, w_aux;
   TuningState() = default;
-  TuningState(long G, long N, long L, double w_init)
-      : w(G * N + G + G * L + L + 2, w_init), w_aux(G * N + G + G * L + L + 2, 0.0) {}
+  // xi_block: G*L with a xi prior (extension; GibbsEngine::tuning_state())
+  TuningState(long G, long N, long L, double w_init, long xi_block = 0)
+      : w(G * N + G + G * L + L + 2 + xi_block, w_init),
+        w_aux(G * N + G + G * L + L + 2 + xi_block, 0.0) {}
 };
 
 // ChainOutput (P:include/countmc/engine.hpp:90-108), accumulators in the
@@ -195,7 +201,9 @@ class GibbsEngine {
     std::vector<double> c = p.c.empty() ? std::vector<double>(p.L, 10.0) : p.c;
     std::vector<double> s = p.s.empty() ? std::vector<double>(p.L, 100.0) : p.s;
     cmc_problem cp{p.G, p.N, p.L, p.counts.data(), p.X.data(), p.h.data(),
-                   p.a, p.b, p.d, c.data(), s.data()};
+                   p.a, p.b, p.d, c.data(), s.data(),
+                   p.beta_prior.empty() ? nullptr : p.beta_prior.data(), p.t_df};
+    for (int v : p.beta_prior) xi_ = xi_ || v != CMC_PRIOR_NORMAL;
     const cmc_run_config cc = cfg.to_c();
     cmc_error e{};
     check(cmc_engine_create(&cp, &cc, contrasts, device, &h_, &e), e);
@@ -212,6 +220,9 @@ class GibbsEngine {
 
   const cmc_run_config& config() const { return cfg_; }
   const std::vector<long>& saved_genes() const { return saved_; }
+
+  // TuningState of this engine's layout at w_init (xi block included)
+  TuningState tuning_state() const { return TuningState(G_, N_, L_, cfg_.w_init, XI()); }
 
   ChainState initial_state(long chain) const {
     ChainState st{G_, N_, L_, std::vector<double>(S())};
@@ -272,8 +283,9 @@ class GibbsEngine {
   void set_progress(Progress fn) { progress_ = std::move(fn); }
 
  private:
-  long S() const { return G_ * N_ + G_ + G_ * L_ + 2 * L_ + 2; }
-  long A() const { return 2 + 2 * L_ + G_ * L_ + G_ + G_ * N_; }
+  long XI() const { return xi_ ? G_ * L_ : 0; }  // trailing xi block (extension)
+  long S() const { return G_ * N_ + G_ + G_ * L_ + 2 * L_ + 2 + XI(); }
+  long A() const { return 2 + 2 * L_ + G_ * L_ + G_ + G_ * N_ + XI(); }
 
   ChainOutput output(long chain) {
     ChainOutput o;
@@ -302,6 +314,7 @@ class GibbsEngine {
   }
 
   cmc_engine* h_ = nullptr;
+  bool xi_ = false;
   cmc_run_config cfg_{};
   long G_, N_, L_;
   long ncols_ = 0, nrows_ = 0;
