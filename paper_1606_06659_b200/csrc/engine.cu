@@ -696,6 +696,7 @@ cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p, int chains,
   if (r != cudaSuccess) return r;
   if ((r = cudaStreamWaitEvent(s, ev_tail, 0)) != cudaSuccess) return r;
   if ((r = launch_gene_sweep(p, chains, off, s)) != cudaSuccess) return r;
+  if (e->xi_any && (r = launch_xi_sweep(p, chains, off, s)) != cudaSuccess) return r;
   if ((r = cudaEventRecord(ev_gene, s)) != cudaSuccess) return r;
   if ((r = cudaStreamWaitEvent(t, ev_gene, 0)) != cudaSuccess) return r;
   if (!e->split_tail) {
@@ -1265,9 +1266,11 @@ void* cmc_engine_stream(cmc_engine* e) {
 
 int cmc_engine_launches_per_sweep(const cmc_engine* e) {
   if (!e) return 0;
+  // per lane: eps, gene, [xi], leaf_a, leaf_b (+ hyper_a/b when split)
   int n = e->split_tail ? 6 : 4;
+  if (e->xi_any) ++n;
   if (e->has_ctab && e->ctab.gene_needs_hyper) ++n;
-  return n;
+  return n * std::max(1, e->n_lanes);
 }
 
 int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,

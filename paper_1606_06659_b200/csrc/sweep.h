@@ -147,6 +147,8 @@ cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
                              cudaStream_t s);
 cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
                               cudaStream_t s);
+cudaError_t launch_xi_sweep(const SweepParams& p, int chains, long m_off,
+                            cudaStream_t s);
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
                           cudaStream_t s);
 cudaError_t launch_hyper_a(const SweepParams& p, int chains, long m_off,

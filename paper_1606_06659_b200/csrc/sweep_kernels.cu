@@ -693,70 +693,27 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
       }
     }
     __syncwarp();
-    auto commit_beta = [&]() {
-      beta[i] = bnew;
-      if (tuning) {
-        beta_w[i] = w;
-        beta_wa[i] = wa;
-      }
-      if (bnew != bold) {
-        for (int j = jb; j < je; ++j) {
-          const double v = __ldg(p.grp_val + j);
-          for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
-            const int n = __ldg(p.grp_mem + q);
-            xs[n * kGeneBlock + tid] += v * (bnew - bold);
-          }
-        }
-      }
-      if (monitor) moments(p.acc_beta + so * 4 * L * G + i, (size_t)L * G, bnew, mcount);
-    };
-    if constexpr (!XI) {
-      if (!alive) continue;
-      if (st) {
-        record_stall(hp, stall_key(5, l, gg, 0), m);
-        alive = false;
-        continue;
-      }
-      commit_beta();
-      continue;
-    }
-    // xi engines: every lane passes the same __syncwarp sequence
-    if (alive && st) {
+    if (!alive) continue;
+    if (st) {
       record_stall(hp, stall_key(5, l, gg, 0), m);
       alive = false;
+      continue;
     }
-    if (alive) commit_beta();
-    if (xcol) {
-      // xi_gl right after beta_gl (extension; reads beta_gl, theta_l and
-      // sigma_l of iteration m-1, like the oracle's step 5)
-      double xnew = 0.0, xw = 0.0, xwa = 0.0;
-      bool xst = false;
-      const size_t ix = so * L * G + i;
-      __syncwarp();
-      if (alive) {
-        const double sg = hp->sigma[l];
-        const double dz = bnew - hp->theta[l];
-        XiF f{p.xi_fam[l], dz * dz / (2.0 * (sg * sg)), p.t_df};
-        xw = p.xi_w[ix];
-        xwa = tuning ? p.xi_wa[ix] : 0.0;
-        Stream rng;
-        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteXi, gg * L + l));
-        xnew = slice_step(f, p.xi[ix], xw, xwa, sc, m, rng, xst);
-      }
-      __syncwarp();
-      if (alive && xst) {
-        record_stall(hp, stall_key(5, l, gg, 1), m);
-        alive = false;
-      }
-      if (alive) {
-        p.xi[ix] = xnew;
-        if (tuning) {
-          p.xi_w[ix] = xw;
-          p.xi_wa[ix] = xwa;
+    beta[i] = bnew;
+    if (tuning) {
+      beta_w[i] = w;
+      beta_wa[i] = wa;
+    }
+    if (bnew != bold) {
+      for (int j = jb; j < je; ++j) {
+        const double v = __ldg(p.grp_val + j);
+        for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
+          const int n = __ldg(p.grp_mem + q);
+          xs[n * kGeneBlock + tid] += v * (bnew - bold);
         }
-        if (monitor) moments(p.acc_xi + so * 4 * L * G + i, (size_t)L * G, xnew, mcount);
       }
     }
+    if (monitor) moments(p.acc_beta + so * 4 * L * G + i, (size_t)L * G, bnew, mcount);
   }
 
   __syncwarp();
@@ -785,6 +742,57 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
     }
   }
   if (clamps) atomicAdd(&hp->clamps, (unsigned long long)clamps);
+}
+
+// xi_gl for every (gene, xi column) of the chain (extension, no reference:
+// parity unpinned).  xi_gl's conditional reads only beta_gl (this sweep),
+// theta_l and sigma_l (iteration m-1), so all G x L steps are independent:
+// one thread per (gene, column) after the gene kernel, grid (G/128, L,
+// chains).  The draws equal the oracle's, which takes xi_gl right after
+// beta_gl inside step 5 (same sites, same inputs); a stall gets key
+// (5, l, g, 1), i.e. after beta_gl and before beta_(g+1)l, the sequential
+// order.
+#ifndef CMC_XI_MIN_BLOCKS
+#define CMC_XI_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(kGeneBlock, CMC_XI_MIN_BLOCKS)
+    xi_sweep_kernel(const SweepParams p, const long m_off) {
+  const int l = blockIdx.y;
+  if (p.xi_fam[l] == CMC_PRIOR_NORMAL) return;  // block-uniform
+  const int slot = p.slot_base + blockIdx.z;
+  Hyper* hp = p.hyper + slot;
+  if (stalled_chain(hp)) return;
+  const long gl = (long)blockIdx.x * kGeneBlock + threadIdx.x;
+  if (gl >= p.G) return;
+  const long m = *p.d_m + m_off;
+  const bool tuning = m <= p.burnin;
+  const int L = p.L;
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const size_t ix = so * L * G + (size_t)l * G + gl;
+  const uint64_t chain = (uint64_t)(p.chain_base + blockIdx.z);
+  const uint64_t gg = (uint64_t)(p.g0 + gl);
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
+  const double sg = hp->sigma[l];
+  const double dz = p.beta[ix] - hp->theta[l];
+  XiF f{p.xi_fam[l], dz * dz / (2.0 * (sg * sg)), p.t_df};
+  double w = p.xi_w[ix];
+  double wa = tuning ? p.xi_wa[ix] : 0.0;
+  Stream rng;
+  rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteXi, gg * L + l));
+  bool st = false;
+  const double x1 = slice_step(f, p.xi[ix], w, wa, sc, m, rng, st);
+  if (st) {
+    record_stall(hp, stall_key(5, l, gg, 1), m);
+    return;
+  }
+  p.xi[ix] = x1;
+  if (tuning) {
+    p.xi_w[ix] = w;
+    p.xi_wa[ix] = wa;
+  }
+  if (p.monitor_enabled && m > p.burnin)
+    moments(p.acc_xi + so * 4 * L * G + (size_t)l * G + gl, (size_t)L * G, x1,
+            (double)(m - p.burnin));
 }
 
 // Serial sum of one 1024-gene leaf by one warp, in gene order: every lane
@@ -1238,6 +1246,12 @@ cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
   }
   if (p.Jmax <= 2) return launch_gene_sweep_t<2, false>(p, chains, m_off, s);
   return launch_gene_sweep_t<0, false>(p, chains, m_off, s);
+}
+
+cudaError_t launch_xi_sweep(const SweepParams& p, int chains, long m_off,
+                            cudaStream_t s) {
+  dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)p.L, (unsigned)chains);
+  return launch_prio(xi_sweep_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_gene, p, m_off);
 }
 
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
