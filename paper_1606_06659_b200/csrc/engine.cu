@@ -525,6 +525,13 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
   CUDA_TRY(put_gn(eps, e->eps.p + so * N * G, N));
   CUDA_TRY(cudaMemcpy(e->gam.p + so * G, gam + g0, sizeof(double) * G,
                       cudaMemcpyHostToDevice));
+  {  // 1/gamma, read by the eps kernel (0.5 * inv_gam = 1/(2 gamma))
+    host_parallel_for(G, [&](long a, long b) {
+      for (long g = a; g < b; ++g) buf[(size_t)g] = 1.0 / gam[g0 + g];
+    });
+    CUDA_TRY(cudaMemcpy(e->inv_gam.p + so * G, buf.data(), sizeof(double) * G,
+                        cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(put_gn(beta, e->beta.p + so * L * G, L));
   if (e->xi_any) CUDA_TRY(put_gn(sigma + L + 2, e->xi.p + so * L * G, L));
   if (tw && ta) {

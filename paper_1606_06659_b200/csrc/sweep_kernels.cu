@@ -487,7 +487,10 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   const double* beta = p.beta + so * L * G;
   double xb = 0.0;
   for (int l = 0; l < L; ++l) xb += __ldg(p.X + n * L + l) * beta[(size_t)l * G + gl];
-  const double inv_two_gam = 1.0 / (2.0 * p.gam[so * G + gl]);
+  // 1/(2 gamma) = 0.5 * RN(1/gamma) exactly (scaling by 2 commutes with
+  // rounding); inv_gam is written with gamma by the gene kernel and by
+  // upload_state, so no divide per (gene, sample)
+  const double inv_two_gam = 0.5 * p.inv_gam[so * G + gl];
   EpsF f{__ldg(p.y + i), __ldg(p.h + n) + xb, inv_two_gam, p.exp_clamp, ExpTab(exp_tab), 0u};
   const double x0 = p.eps[ie];
   double w = p.eps_w[ie];
