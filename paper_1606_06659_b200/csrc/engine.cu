@@ -34,6 +34,7 @@ typedef int (*fn_init_rank)(nccl_comm*, int, nccl_uid, int);
 typedef int (*fn_all_gather)(const void*, void*, size_t, int, nccl_comm,
                              cudaStream_t);
 typedef int (*fn_destroy)(nccl_comm);
+typedef int (*fn_comm_split)(nccl_comm, int, int, nccl_comm*, void*);
 typedef const char* (*fn_errstr)(int);
 
 struct NcclApi {
@@ -42,6 +43,7 @@ struct NcclApi {
   fn_init_rank init_rank = nullptr;
   fn_all_gather all_gather = nullptr;
   fn_destroy destroy = nullptr;
+  fn_comm_split comm_split = nullptr;  // optional (NCCL >= 2.18): per-lane comms
   fn_errstr errstr = nullptr;
   bool load(std::string& why) {
     if (lib) return true;
@@ -58,6 +60,7 @@ struct NcclApi {
     init_rank = (fn_init_rank)dlsym(lib, "ncclCommInitRank");
     all_gather = (fn_all_gather)dlsym(lib, "ncclAllGather");
     destroy = (fn_destroy)dlsym(lib, "ncclCommDestroy");
+    comm_split = (fn_comm_split)dlsym(lib, "ncclCommSplit");
     errstr = (fn_errstr)dlsym(lib, "ncclGetErrorString");
     if (!get_uid || !init_rank || !all_gather || !destroy) {
       why = "libnccl is missing symbols";
@@ -167,6 +170,10 @@ struct DevBuf {
 
 }  // namespace
 
+#ifndef CMC_MAX_LANES
+#define CMC_MAX_LANES 2
+#endif
+
 struct cmc_engine {
   // problem (host copy of the full problem)
   long G_total = 0, N = 0, L = 0;
@@ -190,6 +197,10 @@ struct cmc_engine {
   int rank = 0, world = 1;
   long g0 = 0, G = 0;  // local range
   nccl_comm comm = nullptr;
+  // one communicator per chain lane (lane 0: comm; others split from it), so
+  // the lanes' all-gathers never interleave on one communicator
+  nccl_comm lane_comm[4] = {nullptr, nullptr, nullptr, nullptr};
+  int split_lanes = 1;      // lanes of a sharded engine
   bool split_tail = false;  // NCCL exchange between the leaf and hyper kernels
   // device
   int device = 0;
@@ -249,10 +260,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_gene, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_tail, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
-#ifndef CMC_MAX_LANES
-#define CMC_MAX_LANES 2
-#endif
-  e->n_lanes = e->split_tail ? 1 : (int)std::min<long>(e->C, CMC_MAX_LANES);
+  e->n_lanes = e->split_tail ? e->split_lanes : (int)std::min<long>(e->C, CMC_MAX_LANES);
   {
     for (int k = 0; k < e->n_lanes; ++k) {
       cmc_engine::Lane& ln = e->lanes[k];
@@ -696,31 +704,57 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
 // sweep's eps kernel (which reads only beta and gamma of this sweep) overlaps
 // it, and the next gene kernel waits for ev_tail (it reads nu, tau, theta,
 // sigma).  In a CUDA graph capture the two streams become parallel branches.
-cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p, int chains,
+cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p_in, int chains,
                              long off, cudaStream_t s, cudaStream_t t,
-                             cudaEvent_t ev_gene, cudaEvent_t ev_tail) {
+                             cudaEvent_t ev_gene, cudaEvent_t ev_tail,
+                             nccl_comm comm) {
+  // this launch's chains own a contiguous section of the partial buffers:
+  // [world][chains][Q][lpr] at world * slot_base * Q * lpr
+  SweepParams p = p_in;
+#ifdef CMC_DEBUG_SYNC
+#define DBG_SYNC(what)                                                             \
+  do {                                                                             \
+    cudaError_t d_ = cudaDeviceSynchronize();                                      \
+    std::fprintf(stderr, "[dbg] %s: %s\n", what, cudaGetErrorString(d_));          \
+  } while (0)
+#else
+#define DBG_SYNC(what) \
+  do {                 \
+  } while (0)
+#endif
+  const int Q = leaf_q_a((int)e->L, e->xi_any ? 1 : 0);
+  const size_t lpr = (size_t)p.leaves_per_rank, W = (size_t)e->world;
+#ifndef CMC_BISECT_NOOFF
+  p.partA = e->partA.p + W * (size_t)p.slot_base * Q * lpr;
+  p.partB = e->partB.p + W * (size_t)p.slot_base * e->L * lpr;
+  p.C = chains;
+#endif
+  DBG_SYNC("enter");
   cudaError_t r = launch_eps_sweep(p, chains, off, s);
   if (r != cudaSuccess) return r;
+  DBG_SYNC("eps");
   if ((r = cudaStreamWaitEvent(s, ev_tail, 0)) != cudaSuccess) return r;
   if ((r = launch_gene_sweep(p, chains, off, s)) != cudaSuccess) return r;
+  DBG_SYNC("gene");
   if (e->xi_any && (r = launch_xi_sweep(p, chains, off, s)) != cudaSuccess) return r;
   if ((r = cudaEventRecord(ev_gene, s)) != cudaSuccess) return r;
   if ((r = cudaStreamWaitEvent(t, ev_gene, 0)) != cudaSuccess) return r;
   if (!e->split_tail) {
     if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
+    DBG_SYNC("leaf_a");
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
+    DBG_SYNC("leaf_b");
   } else {
-    const int Q = 2 + (int)e->L + (e->xi_any ? (int)e->L : 0);
-    const size_t cA = (size_t)e->C * Q * p.leaves_per_rank;
-    const size_t cB = (size_t)e->C * e->L * p.leaves_per_rank;
+    const size_t cA = (size_t)chains * Q * lpr;
+    const size_t cB = (size_t)chains * e->L * lpr;
     if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
-    if (g_nccl.all_gather(e->partA.p + (size_t)e->rank * cA, e->partA.p, cA,
-                          kNcclFloat64, e->comm, t) != 0)
+    if (g_nccl.all_gather(p.partA + (size_t)e->rank * cA, p.partA, cA, kNcclFloat64, comm, t) !=
+        0)
       return cudaErrorUnknown;
     if ((r = launch_hyper_a(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
-    if (g_nccl.all_gather(e->partB.p + (size_t)e->rank * cB, e->partB.p, cB,
-                          kNcclFloat64, e->comm, t) != 0)
+    if (g_nccl.all_gather(p.partB + (size_t)e->rank * cB, p.partB, cB, kNcclFloat64, comm, t) !=
+        0)
       return cudaErrorUnknown;
     if ((r = launch_hyper_b(p, chains, off, t)) != cudaSuccess) return r;
   }
@@ -733,7 +767,7 @@ cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p, int chains,
 cudaError_t enqueue_sweep(cmc_engine* e, const SweepParams& p, int chains,
                           long off) {
   return enqueue_sweep_on(e, p, chains, off, e->stream, e->tail_stream, e->ev_gene,
-                          e->ev_tail);
+                          e->ev_tail, e->comm);
 }
 
 // Join the tail stream back into the engine stream (before the iteration
@@ -761,7 +795,8 @@ cudaError_t enqueue_all_lanes(cmc_engine* e, const SweepParams& base, long off) 
     SweepParams p = base;
     p.slot_base = ln.slot0;
     p.chain_base = ln.slot0;
-    cudaError_t r = enqueue_sweep_on(e, p, ln.chains, off, ln.s, ln.t, ln.ev_gene, ln.ev_tail);
+    cudaError_t r = enqueue_sweep_on(e, p, ln.chains, off, ln.s, ln.t, ln.ev_gene, ln.ev_tail,
+                                     k == 0 ? e->comm : e->lane_comm[k]);
     if (r != cudaSuccess) return r;
   }
   return cudaSuccess;
@@ -1045,6 +1080,8 @@ int cmc_engine_destroy(cmc_engine* e) {
     if (e->ev1) cudaEventDestroy(e->ev1);
     cudaStreamDestroy(e->stream);
   }
+  for (int k = 1; k < 4; ++k)
+    if (e->lane_comm[k] && g_nccl.destroy) g_nccl.destroy(e->lane_comm[k]);
   if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
   delete e;
   return CMC_OK;
@@ -1713,6 +1750,16 @@ int cmc_engine_shard(cmc_engine* e, int rank, int world, const void* uid,
       return CMC_ERR_NCCL;
     }
     e->split_tail = true;
+    // chain lanes: one split communicator per extra lane (collective; every
+    // rank has the same chain count, hence the same lane count)
+    e->split_lanes = 1;
+    const int want = (int)std::min<long>(e->C, CMC_MAX_LANES);
+    if (want > 1 && g_nccl.comm_split) {
+      int k = 1;
+      for (; k < want; ++k)
+        if (g_nccl.comm_split(e->comm, 0, rank, &e->lane_comm[k], nullptr) != 0) break;
+      e->split_lanes = k;
+    }
   }
   return CMC_OK;
 }

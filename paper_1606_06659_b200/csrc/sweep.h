@@ -18,7 +18,11 @@ namespace cmc {
 
 constexpr int kLMax = 16;         // model-matrix columns supported
 constexpr int kLeaf = 1024;       // reference reduction leaf, P:include/countmc/parallel.hpp:60
-constexpr int kGeneBlock = 128;   // threads (= genes) per sweep block
+constexpr int kGeneBlock = 128;   // threads (= genes) per eps / xi block
+#ifndef CMC_GENE_THREADS
+#define CMC_GENE_THREADS 128
+#endif
+constexpr int kGeneThreads = CMC_GENE_THREADS;  // threads (= genes) per gene block
 constexpr int kMaxContrasts = 8;
 constexpr int kMaxTerms = 32;
 constexpr int kMaxCoefs = 64;
@@ -117,9 +121,12 @@ struct SweepParams {
   double* samples;  // [C][n_cols][n_rows]
   const int* saved_slot;  // [G] local: saved index or -1
   // reductions
-  double* partA;  // [world][C][Q][leaves_per_rank], Q = leaf_q_a(L, xi_any)
-  double* partB;  // [world][C][L][leaves_per_rank]
-  int C;          // chains resident (stride of the partial buffers)
+  // Leaf partials of THIS launch's chains (one lane): [world][C][Q][lpr]
+  // and [world][C][L][lpr], indexed by slot - slot_base, so each lane's
+  // block is contiguous per rank and one all-gather moves it.
+  double* partA;  // Q = leaf_q_a(L, xi_any)
+  double* partB;
+  int C;          // chains of this launch's lane (stride of the partial buffers)
   // optional block timeline (debug/profiling): per record {kernel<<56 |
   // slot<<48 | smid<<32 | blockIdx.x, t_start_ns, t_end_ns}
   unsigned long long* trace;

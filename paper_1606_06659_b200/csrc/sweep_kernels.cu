@@ -26,6 +26,8 @@
 
 #include "fastmath.cuh"
 #include "rng.cuh"
+#include <cassert>
+
 #include "sweep.h"
 
 namespace cmc {
@@ -258,7 +260,7 @@ struct SigmaF {
 struct BetaF {
   double a, theta, inv_two_sig2, e700;
   const double* val;   // group values (uniform across the warp)
-  const double* S;     // shared memory, stride kGeneBlock
+  const double* S;     // shared memory, stride kGeneThreads
   const double* logS;
   ExpTab tab;
   int J;
@@ -267,8 +269,8 @@ struct BetaF {
     double tot = a * b;
     for (int j = 0; j < J; ++j) {
       const double t = val[j] * b;
-      const double lS = logS[j * kGeneBlock];
-      const double Sj = S[j * kGeneBlock];
+      const double lS = logS[j * kGeneThreads];
+      const double Sj = S[j * kGeneThreads];
       if (lS + t > kExpClamp) {
         ++clamps;
         tot -= e700;
@@ -396,24 +398,33 @@ __device__ __forceinline__ void record_stall(Hyper* hp, unsigned long long key,
   hp->err_m = m;
 }
 
-// Accessor for the gathered leaf partials: [rank][C][Q][leaves_per_rank].
-__device__ __forceinline__ double leaf_part(const double* part,
-                                            const SweepParams& p, int slot,
-                                            int Q, int q, long leaf) {
-  const long lpr = p.leaves_per_rank;
-  const long r = leaf / lpr, j = leaf % lpr;
-  return __ldcg(part + (((r * p.C + slot) * Q + q) * lpr + j));
+// Accessor for the gathered leaf partials of one lane:
+// [rank][C][Q][leaves_per_rank], chain index relative to the lane.  Plain
+// scalars, not the SweepParams: a reference to the kernel's parameter
+// block inside the noinline recursion below would copy the whole block to
+// the stack.
+struct PartView {
+  const double* part;
+  long C, c, Q, lpr;  // lane chains, this chain (relative), quantities, leaves/rank
+};
+__device__ __forceinline__ PartView part_view(const double* part, const SweepParams& p,
+                                              int slot, int Q) {
+  return PartView{part, p.C, slot - p.slot_base, Q, p.leaves_per_rank};
+}
+__device__ __forceinline__ double leaf_part(const PartView& v, int q, long leaf) {
+  const long r = leaf / v.lpr, j = leaf % v.lpr;
+#ifdef CMC_DEBUG_BOUNDS
+  assert(v.c >= 0 && v.c < v.C && q < v.Q);
+#endif
+  return __ldcg(v.part + (((r * v.C + v.c) * v.Q + q) * v.lpr + j));
 }
 
 // pairwise_sum over the leaf partials, P:src/parallel.cpp:81-86.
-__device__ __noinline__ double pairwise_leaves(const double* part,
-                                               const SweepParams& p, int slot,
-                                               int Q, int q, long lo, long n) {
+__device__ __noinline__ double pairwise_leaves(const PartView v, int q, long lo, long n) {
   if (n == 0) return 0.0;
-  if (n == 1) return leaf_part(part, p, slot, Q, q, lo);
+  if (n == 1) return leaf_part(v, q, lo);
   const long mid = n / 2;
-  return pairwise_leaves(part, p, slot, Q, q, lo, mid) +
-         pairwise_leaves(part, p, slot, Q, q, lo + mid, n - mid);
+  return pairwise_leaves(v, q, lo, mid) + pairwise_leaves(v, q, lo + mid, n - mid);
 }
 
 __device__ double param_value(const ContrastTable* t, int k, const double* beta,
@@ -531,7 +542,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 // XI: some column has a xi prior (extension); the reference model (all
 // normal) is compiled without the xi step.
 template <int JR, bool XI>
-__global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
+__global__ void __launch_bounds__(kGeneThreads, CMC_GENE_MIN_BLOCKS)
     gene_sweep_kernel(const SweepParams p, const long m_off) {
   extern __shared__ double smem[];
   __shared__ double exp_tab[32];
@@ -543,7 +554,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
   if (stalled_chain(hp)) return;  // warp-uniform: one load per warp
-  const long gl_raw = (long)blockIdx.x * kGeneBlock + tid;
+  const long gl_raw = (long)blockIdx.x * kGeneThreads + tid;
   bool alive = gl_raw < p.G;
   const long gl = alive ? gl_raw : 0;
 
@@ -563,25 +574,25 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
   double* beta_w = p.beta_w + so * L * G;
   double* beta_wa = p.beta_wa + so * L * G;
   double* xs = smem;                             // [N][B]: lp
-  double* sS = smem + (size_t)N * kGeneBlock;    // [Jmax][B]
-  double* sLogS = sS + (size_t)p.Jmax * kGeneBlock;
+  double* sS = smem + (size_t)N * kGeneThreads;    // [Jmax][B]
+  double* sLogS = sS + (size_t)p.Jmax * kGeneThreads;
   unsigned clamps = 0;
 
   // lp_n = (h_n + eps_n) + xb_n with the new eps and the previous beta,
   // and ss = sum_n eps_n^2 in n order (P:src/engine.cpp:275-283,
   // P:src/model.cpp:76-82)
-  for (int n = 0; n < N; ++n) xs[n * kGeneBlock + tid] = 0.0;
+  for (int n = 0; n < N; ++n) xs[n * kGeneThreads + tid] = 0.0;
   for (int l = 0; l < L; ++l) {
     const double b = alive ? beta[(size_t)l * G + gl] : 0.0;
     for (int n = 0; n < N; ++n)
-      xs[n * kGeneBlock + tid] += __ldg(p.X + n * L + l) * b;
+      xs[n * kGeneThreads + tid] += __ldg(p.X + n * L + l) * b;
   }
   const double gam_old = alive ? p.gam[so * G + gl] : 1.0;
   double ss = 0.0;
   for (int n = 0; n < N; ++n) {
     const double e = alive ? eps[(size_t)n * G + gl] : 0.0;
     ss += e * e;
-    xs[n * kGeneBlock + tid] = __ldg(p.h + n) + e + xs[n * kGeneBlock + tid];
+    xs[n * kGeneThreads + tid] = __ldg(p.h + n) + e + xs[n * kGeneThreads + tid];
   }
 
   // Step 2: gamma_g, P:src/engine.cpp:204-226 (nu, tau of iteration m-1)
@@ -642,7 +653,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
         double s = 0.0;
         for (int q = q0; q < q1; ++q) {
           const int n = __ldg(p.grp_mem + q);
-          double t = xs[n * kGeneBlock + tid] - vb;
+          double t = xs[n * kGeneThreads + tid] - vb;
           if (t > kExpClamp) {
             ++clamps;
             t = kExpClamp;
@@ -686,8 +697,8 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
       } else {
         for (int j = jb; j < je; ++j) {
           const double s = group_sum(j);
-          sS[(j - jb) * kGeneBlock + tid] = s;
-          sLogS[(j - jb) * kGeneBlock + tid] = log(s);
+          sS[(j - jb) * kGeneThreads + tid] = s;
+          sLogS[(j - jb) * kGeneThreads + tid] = log(s);
         }
         BetaF f{__ldg(p.A + i), hp->theta[l], inv2v, p.exp_clamp,
                 p.grp_val + jb, sS + tid, sLogS + tid, etab, je - jb, 0u};
@@ -712,7 +723,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_GENE_MIN_BLOCKS)
         const double v = __ldg(p.grp_val + j);
         for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
           const int n = __ldg(p.grp_mem + q);
-          xs[n * kGeneBlock + tid] += v * (bnew - bold);
+          xs[n * kGeneThreads + tid] += v * (bnew - bold);
         }
       }
     }
@@ -838,8 +849,7 @@ __device__ __noinline__ double pairwise_rec(const double* x, int n) {
 // internal nodes above are rebuilt with shuffles as left + right.  A node of
 // size 1 passes its single leaf through and a node of size 0 is 0.0, as the
 // reference recursion returns them, so the result is bit-identical.
-__device__ double warp_pairwise_leaves(const double* part, const SweepParams& p,
-                                       int slot, int Q, int q, int n) {
+__device__ double warp_pairwise_leaves(const PartView pv, int q, int n) {
   const int lane = threadIdx.x & 31;
   int lo = 0, cnt = n;
   int cnts[5];
@@ -857,10 +867,10 @@ __device__ double warp_pairwise_leaves(const double* part, const SweepParams& p,
   double v;
   if (cnt <= 64) {
     double buf[64];
-    for (int i = 0; i < cnt; ++i) buf[i] = leaf_part(part, p, slot, Q, q, lo + i);
+    for (int i = 0; i < cnt; ++i) buf[i] = leaf_part(pv, q, lo + i);
     v = pairwise_rec(buf, cnt);
   } else {
-    v = pairwise_leaves(part, p, slot, Q, q, lo, cnt);
+    v = pairwise_leaves(pv, q, lo, cnt);
   }
 #pragma unroll
   for (int d = 4; d >= 0; --d) {
@@ -891,12 +901,12 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
   if constexpr (!XI) {
     (void)nwarps;
     if (warp < Q) {
-      const double r = warp_pairwise_leaves(p.partA, p, slot, Q, warp, p.n_leaves_total);
+      const double r = warp_pairwise_leaves(part_view(p.partA, p, slot, Q), warp, p.n_leaves_total);
       if ((tid & 31) == 0) red[warp] = r;
     }
   } else {  // Q = 2 + 2L may exceed the block's 32 warps
     for (int q = warp; q < Q; q += nwarps) {
-      const double r = warp_pairwise_leaves(p.partA, p, slot, Q, q, p.n_leaves_total);
+      const double r = warp_pairwise_leaves(part_view(p.partA, p, slot, Q), q, p.n_leaves_total);
       if ((tid & 31) == 0) red[q] = r;
     }
   }
@@ -974,7 +984,7 @@ __device__ void hyper_b_body(const SweepParams& p, int slot, long m) {
   const int L = p.L;
   const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   if (warp < L) {
-    const double r = warp_pairwise_leaves(p.partB, p, slot, L, warp, p.n_leaves_total);
+    const double r = warp_pairwise_leaves(part_view(p.partB, p, slot, L), warp, p.n_leaves_total);
     if ((tid & 31) == 0) red[warp] = r;
   }
   __syncthreads();
@@ -1074,7 +1084,7 @@ __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
                           : warp == 1 ? p.inv_gam + so * G
                                       : p.beta + so * L * G + (size_t)(warp - 2) * G;
       const double s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
-      if (lane == 0) p.partA[((rank * p.C + slot) * Q + warp) * lpr + lb] = s;
+      if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Q + warp) * lpr + lb] = s;
     }
   } else {
     // xi engine: quantities [log gamma, 1/gamma, S_l, W_l] (sweep.h), looped
@@ -1096,7 +1106,7 @@ __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
         const double* xs = p.xi + so * L * G + (size_t)(q - 2 - L) * G;
         s = warp_leaf_sum([&](long i) { return 1.0 / xs[i]; }, start, end);
       }
-      if (lane == 0) p.partA[((rank * p.C + slot) * Q + q) * lpr + lb] = s;
+      if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Q + q) * lpr + lb] = s;
     }
   }
   if (!p.fuse_tail) return;
@@ -1146,7 +1156,7 @@ __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
     if (lane == 0) {
       const long lpr = p.leaves_per_rank;
       const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
-      p.partB[((rank * p.C + slot) * L + warp) * lpr + lb] = s;
+      p.partB[((rank * p.C + (slot - p.slot_base)) * L + warp) * lpr + lb] = s;
     }
   }
   if (!p.fuse_tail) return;
@@ -1216,7 +1226,7 @@ cudaError_t launch_prio(K kernel, dim3 grid, dim3 block, size_t smem,
 }
 
 int gene_sweep_smem_bytes(int N, int Jmax) {
-  return (int)(sizeof(double) * (size_t)(N + 2 * Jmax) * kGeneBlock);
+  return (int)(sizeof(double) * (size_t)(N + 2 * Jmax) * kGeneThreads);
 }
 
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
@@ -1236,8 +1246,8 @@ static cudaError_t launch_gene_sweep_t(const SweepParams& p, int chains, long m_
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)chains);
-  return launch_prio(gene_sweep_kernel<JR, XI>, grid, dim3(kGeneBlock), smem, s, p.prio_gene, p,
+  dim3 grid((unsigned)((p.G + kGeneThreads - 1) / kGeneThreads), (unsigned)chains);
+  return launch_prio(gene_sweep_kernel<JR, XI>, grid, dim3(kGeneThreads), smem, s, p.prio_gene, p,
                      m_off);
 }
 

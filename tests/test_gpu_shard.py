@@ -62,3 +62,26 @@ def test_exchange_path_iterate_matches_oracle():
         assert not len(mismatch(p[keep], st[keep])), m
         np.testing.assert_allclose(p[th], st[th], rtol=1e-12)
         assert np.array_equal(tu.w, tw) and np.array_equal(tu.w_aux, ta)
+
+
+def test_exchange_path_two_lanes_with_xi_prior():
+    """Four chains: the sharded engine runs two chain lanes, each with its
+    own split communicator and its own section of the partial buffers; a xi
+    prior adds the xi kernel and the 2 + 2L leaf quantities.  Bit-identical
+    to the fused path."""
+    from paper_1606_06659_b200 import PriorConfig
+    counts, X, h = heterosis(2100, seed=8)
+    cfg = RunConfig(chains=4, burnin=20, iterations=30, thin=10, seed=9, save_genes=4)
+    spec = lambda: ModelSpec(X, h, PriorConfig(beta_prior=["normal", "laplace", "t",  # noqa: E731
+                                                           "horseshoe", "normal"], t_df=3.0))
+    fused = GibbsEngine(CountMatrix(counts), spec(), cfg, contrasts=[heterosis_contrast()])
+    shard = GibbsEngine(CountMatrix(counts), spec(), cfg, contrasts=[heterosis_contrast()])
+    shard.shard(0, 1, GibbsEngine.nccl_unique_id())
+    a, b = fused.run(), shard.run()
+    # per lane: eps, gene, xi, leaf_a, hyper_a, leaf_b, hyper_b
+    assert shard._lib.cmc_engine_launches_per_sweep(shard.handle) == 2 * 7
+    for c in range(4):
+        assert np.array_equal(a[c].final_state.pack(), b[c].final_state.pack()), c
+        assert np.array_equal(a[c].xi_acc.mean, b[c].xi_acc.mean)
+        assert np.array_equal(a[c].sigma_acc.mean, b[c].sigma_acc.mean)
+        assert np.array_equal(a[c].contrasts[0].prob, b[c].contrasts[0].prob)
