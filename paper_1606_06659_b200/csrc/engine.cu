@@ -1336,6 +1336,7 @@ int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
     CUDA_TRY(cudaEventRecord(ev[3 * r], e->stream));
     CUDA_TRY(launch_eps_sweep(p, e->C, r, e->stream));
     CUDA_TRY(launch_gene_sweep(p, e->C, r, e->stream));
+    if (e->xi_any) CUDA_TRY(launch_xi_sweep(p, e->C, r, e->stream));
     CUDA_TRY(cudaEventRecord(ev[3 * r + 1], e->stream));
     SweepParams q = p;
     // the tail: everything enqueue_sweep launches after the gene kernel
