@@ -227,6 +227,7 @@ struct cmc_engine {
   DevBuf<double> log_gam, inv_gam, acc_eps, acc_gam, acc_beta, cprob, samples;
   DevBuf<double> partA, partB;
   DevBuf<double> xi, xi_w, xi_wa, acc_xi;  // [C][L][G] (acc: [C][4][L][G])
+  DevBuf<double> xfer;  // max(N, L) x G: layout transposes for host transfers
   DevBuf<Hyper> hyper;
   DevBuf<ContrastTable> dctab;
   DevBuf<long> d_m;
@@ -350,6 +351,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(e->samples.alloc(std::max<long>(1, e->n_cols * e->n_rows) * C));
   CUDA_TRY(e->hyper.alloc((size_t)C));
   CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * C));
+  CUDA_TRY(e->xfer.alloc((size_t)std::max(N, L) * G));
   const long n_leaves_total = (e->G_total + kLeaf - 1) / kLeaf;
   const long lpr = (n_leaves_total + e->world - 1) / e->world;
   CUDA_TRY(e->partA.alloc((size_t)e->world * C * Q * lpr));
@@ -512,6 +514,26 @@ void initial_state_host(const cmc_engine* e, long chain, double* st) {
   if (e->xi_any) std::fill(sigma + L + 2, sigma + L + 2 + G * L, 1.0);  // xi block
 }
 
+// Host AoS block [G_local][K] (the reference's row-major layout) <-> device
+// SoA [K][G_local]: one contiguous copy plus a device transpose through
+// e->xfer, ordered on the engine stream (the caller synchronises).
+cudaError_t aos_to_device(cmc_engine* e, const double* src_aos, double* dst_soa, long K) {
+  const long G = e->G;
+  cudaError_t r = cudaMemcpyAsync(e->xfer.p, src_aos, sizeof(double) * K * G,
+                                  cudaMemcpyHostToDevice, e->stream);
+  if (r != cudaSuccess) return r;
+  return launch_transpose(e->xfer.p, dst_soa, G, (int)K, false, e->stream);
+}
+cudaError_t device_to_aos(cmc_engine* e, const double* src_soa, double* dst_aos, long K) {
+  const long G = e->G;
+  cudaError_t r = launch_transpose(src_soa, e->xfer.p, G, (int)K, true, e->stream);
+  if (r != cudaSuccess) return r;
+  r = cudaMemcpyAsync(dst_aos, e->xfer.p, sizeof(double) * K * G, cudaMemcpyDeviceToHost,
+                      e->stream);
+  if (r != cudaSuccess) return r;
+  return cudaStreamSynchronize(e->stream);  // the staging buffer is reused next
+}
+
 // Upload one chain's packed state (+ optional tuning) into slot `c`.
 int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
                  const double* ta, cmc_error* err) {
@@ -523,11 +545,9 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
   const double* sigma = theta + L;
   std::vector<double> buf((size_t)std::max(N, L) * G);
   auto put_gn = [&](const double* src, double* dst, long K) -> cudaError_t {
-    host_parallel_for(G, [&](long a, long b) {
-      for (long g = a; g < b; ++g)
-        for (long k = 0; k < K; ++k) buf[(size_t)k * G + g] = src[(g0 + g) * K + k];
-    });
-    return cudaMemcpy(dst, buf.data(), sizeof(double) * K * G, cudaMemcpyHostToDevice);
+    cudaError_t r = aos_to_device(e, src + g0 * K, dst, K);
+    if (r != cudaSuccess) return r;
+    return cudaStreamSynchronize(e->stream);  // e->xfer is reused by the next call
   };
   const size_t so = (size_t)c;
   CUDA_TRY(put_gn(eps, e->eps.p + so * N * G, N));
@@ -588,16 +608,8 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
 int download_state(cmc_engine* e, long c, double* st, double* tw, double* ta,
                    cmc_error* err) {
   const long Gt = e->G_total, G = e->G, N = e->N, L = e->L, g0 = e->g0;
-  std::vector<double> buf((size_t)std::max(N, L) * G);
   auto get_gn = [&](const double* src, double* dst, long K) -> cudaError_t {
-    cudaError_t r = cudaMemcpy(buf.data(), src, sizeof(double) * K * G,
-                               cudaMemcpyDeviceToHost);
-    if (r != cudaSuccess) return r;
-    host_parallel_for(G, [&](long a, long b) {
-      for (long g = a; g < b; ++g)
-        for (long k = 0; k < K; ++k) dst[(g0 + g) * K + k] = buf[(size_t)k * G + g];
-    });
-    return cudaSuccess;
+    return device_to_aos(e, src, dst + g0 * K, K);
   };
   const size_t so = (size_t)c;
   Hyper hp;
@@ -1632,43 +1644,26 @@ int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,
     dst[i++] = hp.acc[k][1];
     for (long l = 0; l < L; ++l) dst[i++] = hp.acc[k][2 + l];
     for (long l = 0; l < L; ++l) dst[i++] = hp.acc[k][2 + L + l];
-    // beta G x L
-    buf.resize((size_t)L * G);
-    CUDA_TRY(cudaMemcpy(buf.data(), e->acc_beta.p + so * 4 * L * G + (size_t)k * L * G,
-                        sizeof(double) * L * G, cudaMemcpyDeviceToHost));
-    host_parallel_for(G, [&](long a, long b) {
-      for (long g = a; g < b; ++g)
-        for (long l = 0; l < L; ++l) dst[i + (g0 + g) * L + l] = buf[(size_t)l * G + g];
-    });
+    // beta G x L, gamma G, eps G x N: device transpose, one copy each
+    CUDA_TRY(device_to_aos(e, e->acc_beta.p + so * 4 * L * G + (size_t)k * L * G,
+                           dst + i + g0 * L, L));
     i += Gt * L;
-    buf.resize((size_t)G);
-    CUDA_TRY(cudaMemcpy(buf.data(), e->acc_gam.p + so * 4 * G + (size_t)k * G,
+    CUDA_TRY(cudaMemcpy(dst + i + g0, e->acc_gam.p + so * 4 * G + (size_t)k * G,
                         sizeof(double) * G, cudaMemcpyDeviceToHost));
-    for (long g = 0; g < G; ++g) dst[i + g0 + g] = buf[(size_t)g];
     i += Gt;
-    buf.resize((size_t)N * G);
-    CUDA_TRY(cudaMemcpy(buf.data(), e->acc_eps.p + so * 4 * N * G + (size_t)k * N * G,
-                        sizeof(double) * N * G, cudaMemcpyDeviceToHost));
-    host_parallel_for(G, [&](long a, long b) {
-      for (long g = a; g < b; ++g)
-        for (long n = 0; n < N; ++n) dst[i + (g0 + g) * N + n] = buf[(size_t)n * G + g];
-    });
+    CUDA_TRY(device_to_aos(e, e->acc_eps.p + so * 4 * N * G + (size_t)k * N * G,
+                           dst + i + g0 * N, N));
     i += Gt * N;
     if (e->xi_any) {
       // xi block (extension): sampled columns from the device; a normal
       // column's xi is the constant 1, whose compensated Welford state after
       // `count` updates is (1, 1, 0, 0)
-      buf.resize((size_t)L * G);
-      CUDA_TRY(cudaMemcpy(buf.data(), e->acc_xi.p + so * 4 * L * G + (size_t)k * L * G,
-                          sizeof(double) * L * G, cudaMemcpyDeviceToHost));
+      CUDA_TRY(device_to_aos(e, e->acc_xi.p + so * 4 * L * G + (size_t)k * L * G,
+                             dst + i + g0 * L, L));
       const double konst = (k < 2 && count > 0) ? 1.0 : 0.0;
-      host_parallel_for(G, [&](long a, long b) {
-        for (long g = a; g < b; ++g)
-          for (long l = 0; l < L; ++l)
-            dst[i + (g0 + g) * L + l] = e->prior[(size_t)l] != CMC_PRIOR_NORMAL
-                                            ? buf[(size_t)l * G + g]
-                                            : konst;
-      });
+      for (long l = 0; l < L; ++l)
+        if (e->prior[(size_t)l] == CMC_PRIOR_NORMAL)
+          for (long g = 0; g < G; ++g) dst[i + (g0 + g) * L + l] = konst;
     }
   }
   if (e->has_ctab) {

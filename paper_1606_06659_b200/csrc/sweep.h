@@ -171,6 +171,9 @@ cudaError_t launch_fastmath_setup(cudaStream_t s);
 cudaError_t launch_compute_A(const double* y, const double* X, double* A,
                              int G, int N, int L, cudaStream_t s);
 int gene_sweep_smem_bytes(int N, int Jmax);
+// [K][G] <-> [G][K] (to_aos: SoA -> AoS) on the device
+cudaError_t launch_transpose(const double* src, double* dst, long G, int K, bool to_aos,
+                             cudaStream_t s);
 
 }  // namespace cmc
 

@@ -1261,6 +1261,58 @@ cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
   return launch_gene_sweep_t<0, false>(p, chains, m_off, s);
 }
 
+// Layout transposes for state/output transfer: SoA [K][G] <-> the
+// reference's AoS [G][K], through a 32-gene shared tile so both sides are
+// coalesced (the host then moves one contiguous block).
+__global__ void soa_to_aos_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                  long G, int K) {
+  __shared__ double tile[32][65];
+  const long g0 = (long)blockIdx.x * 32;
+  for (int k0 = 0; k0 < K; k0 += 64) {
+    const int kn = min(64, K - k0);
+    for (int i = threadIdx.x; i < 32 * kn; i += blockDim.x) {
+      const int k = i / 32, j = i % 32;
+      if (g0 + j < G) tile[j][k] = src[(size_t)(k0 + k) * G + g0 + j];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * kn; i += blockDim.x) {
+      const int j = i / kn, k = i % kn;
+      if (g0 + j < G) dst[(size_t)(g0 + j) * K + k0 + k] = tile[j][k];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void aos_to_soa_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                  long G, int K) {
+  __shared__ double tile[32][65];
+  const long g0 = (long)blockIdx.x * 32;
+  for (int k0 = 0; k0 < K; k0 += 64) {
+    const int kn = min(64, K - k0);
+    for (int i = threadIdx.x; i < 32 * kn; i += blockDim.x) {
+      const int j = i / kn, k = i % kn;
+      if (g0 + j < G) tile[j][k] = src[(size_t)(g0 + j) * K + k0 + k];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * kn; i += blockDim.x) {
+      const int k = i / 32, j = i % 32;
+      if (g0 + j < G) dst[(size_t)(k0 + k) * G + g0 + j] = tile[j][k];
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_transpose(const double* src, double* dst, long G, int K, bool to_aos,
+                             cudaStream_t s) {
+  if (G <= 0 || K <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((G + 31) / 32);
+  if (to_aos)
+    soa_to_aos_kernel<<<blocks, 256, 0, s>>>(src, dst, G, K);
+  else
+    aos_to_soa_kernel<<<blocks, 256, 0, s>>>(src, dst, G, K);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_xi_sweep(const SweepParams& p, int chains, long m_off,
                             cudaStream_t s) {
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)p.L, (unsigned)chains);

@@ -10,7 +10,7 @@ G, N = 39656, 16
 X = builtin_design("heterosis16x5", N)
 counts = generate(SimSpec(G=G, N=N, X=X, nu=8, tau=0.7, theta=[2.5,.2,.2,0,.1], sigma=[.4,.25,.25,.15,.2], seed=1)).counts
 import torch; torch.cuda.init(); torch.zeros(1, device="cuda")
-for B, E in [(200, 500), (2000, 4000)]:
+for B, E in [(200, 500), (2000, 4000), (2000, 4000), (2000, 4000)]:
     t0 = time.perf_counter()
     eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, np.zeros(N)), RunConfig(chains=4, burnin=B, iterations=E, thin=20, seed=7), contrasts=[heterosis_contrast()])
     t1 = time.perf_counter()
