@@ -1245,7 +1245,10 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
   p.chain_base = 0;
   p.monitor_enabled = 1;
   const long total = m_end - m_begin;
-  const long chunk = 25;
+#ifndef CMC_GRAPH_CHUNK
+#define CMC_GRAPH_CHUNK 50  // sweeps per CUDA graph (A/B: 25 0.3551 ms, 50 0.3531, 100 0.3527)
+#endif
+  const long chunk = CMC_GRAPH_CHUNK;
   CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
   long done = 0;
   if (total >= chunk) {
