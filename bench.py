@@ -251,7 +251,8 @@ def run_b200(a, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     value = C * G * K / (ms * 1e-3)
-    launches = K * lib.cmc_engine_launches_per_sweep(hd) + (K // 25) + (1 if K % 25 else 0)
+    # per-sweep kernels of every lane + one iteration-advance kernel per 50-sweep graph
+    launches = K * lib.cmc_engine_launches_per_sweep(hd) + (K // 50) + (1 if K % 50 else 0)
 
     # dominant kernel timed live with events on the engine stream
     gene_ms, tail_ms = c_double(), c_double()
