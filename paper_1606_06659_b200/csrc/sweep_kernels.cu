@@ -1122,6 +1122,7 @@ __global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
 }
 
 // Leaf sums of (beta_l - theta_l)^2 with theta of this iteration.
+template <bool XI>
 __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
   WarpTrace wt(p, 4, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
@@ -1137,7 +1138,7 @@ __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
     const double th = hp->theta[warp];
     const double* src = p.beta + so * L * G + (size_t)warp * G;
     double s;
-    if (p.xi_any && p.xi_fam[warp] != CMC_PRIOR_NORMAL) {  // extension: /xi
+    if (XI && p.xi_fam[warp] != CMC_PRIOR_NORMAL) {  // extension: /xi
       const double* xs = p.xi + so * L * G + (size_t)warp * G;
       s = warp_leaf_sum(
           [&](long i) {
@@ -1345,7 +1346,11 @@ cudaError_t launch_leaf_b(const SweepParams& p, int chains, long m_off,
                           cudaStream_t s) {
   const int threads = 32 * (p.L > 1 ? p.L : 1);
   dim3 grid((unsigned)p.n_leaves_local, (unsigned)chains);
-  return launch_prio(leaf_b_kernel, grid, dim3(threads < 32 ? 32 : threads), 0, s, p.prio_tail, p, m_off);
+  if (p.xi_any)
+    return launch_prio(leaf_b_kernel<true>, grid, dim3(threads < 32 ? 32 : threads), 0, s,
+                       p.prio_tail, p, m_off);
+  return launch_prio(leaf_b_kernel<false>, grid, dim3(threads < 32 ? 32 : threads), 0, s,
+                     p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_hyper_b(const SweepParams& p, int chains, long m_off,
