@@ -492,6 +492,15 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   const size_t i = (size_t)n * G + gl;
   const size_t ie = so * N * G + i;
+  const bool monitor = p.monitor_enabled && m > p.burnin;
+  double* acc = p.acc_eps + so * 4 * N * G + i;
+  if (monitor) {
+    // the four Welford words come from HBM: start them towards L2 now so the
+    // update after the slice step does not wait on DRAM
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(acc + (size_t)k * N * G));
+  }
 
   // xb_gn = sum_l X_nl beta_gl, l ascending from 0.0 (refresh_xb,
   // P:src/engine.cpp:144-159)
@@ -522,8 +531,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
       p.eps_w[ie] = w;
       p.eps_wa[ie] = wa;
     }
-    if (p.monitor_enabled && m > p.burnin)
-      moments(p.acc_eps + so * 4 * N * G + i, (size_t)N * G, x1, (double)(m - p.burnin));
+    if (monitor) moments(acc, (size_t)N * G, x1, (double)(m - p.burnin));
   }
   if (f.clamps) atomicAdd(&hp->clamps, (unsigned long long)f.clamps);
 }
