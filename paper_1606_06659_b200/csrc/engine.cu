@@ -971,6 +971,16 @@ int cmc_engine_create(const cmc_problem* p, const cmc_run_config* config,
     jmax = std::max<int>(jmax, (int)vals.size());
   }
   e->Jmax = jmax;
+  {
+    // the gene kernel keeps lp (N) and, beyond 2 groups per column, the
+    // group sums (2 Jmax) per gene in shared memory
+    const int smem = gene_sweep_smem_bytes((int)p->N, jmax <= 2 ? 0 : jmax);
+    if (smem > 227 * 1024) {
+      delete e;
+      return fail_config(err, "N (plus 2x the groups per model-matrix column) too large for "
+                              "this build's gene kernel: at most 227 samples");
+    }
+  }
 
   // saved genes: partial Fisher-Yates on (seed, 0, 0, kSaveSel), sorted,
   // P:src/engine.cpp:77-90

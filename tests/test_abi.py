@@ -125,3 +125,17 @@ def test_simulate_is_deterministic_and_shaped():
     assert a.dtype == np.int64 and a.min() >= 0 and a.shape == (100, 16)
     # log-mean near theta_1 = 2.5 on average over genes
     assert 1.5 < np.log(a.mean(axis=1) + 1).mean() < 3.5
+
+
+def test_sample_count_beyond_gene_kernel_shared_memory():
+    """The gene kernel keeps lp (N doubles per gene) in shared memory: a
+    clear ConfigError at create, not a launch failure later."""
+    from paper_1606_06659_b200 import builtin_design
+    X = builtin_design("heterosis16x5", 240)
+    counts = np.ones((8, 240), np.int64)
+    with pytest.raises(ConfigError, match="at most 227 samples"):
+        GibbsEngine(CountMatrix(counts), ModelSpec(X, np.zeros(240)),
+                    RunConfig(chains=1, burnin=10, iterations=10))
+    X = builtin_design("heterosis16x5", 224)   # fits
+    GibbsEngine(CountMatrix(np.ones((8, 224), np.int64)), ModelSpec(X, np.zeros(224)),
+                RunConfig(chains=1, burnin=10, iterations=10))
