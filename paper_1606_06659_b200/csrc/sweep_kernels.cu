@@ -1476,7 +1476,11 @@ __global__ void diag_rows_kernel(const DiagParams d) {
 // reference's serial order, lane 0 runs the Geyer initial-positive,
 // monotone pair scan.
 __global__ void diag_ess_kernel(const DiagParams d) {
-  extern __shared__ double lagc[];  // [n_rows] autocovariances
+  // lags are computed 64 at a time (two per lane) and lane 0 runs the
+  // Geyer scan over each batch, stopping where the reference stops: cost
+  // O(M x cutoff) like avg_autocov on demand, and O(1) shared memory
+  __shared__ double lagb[64];
+  __shared__ double mu[32];
   const long col = blockIdx.x;
   const int lane = threadIdx.x;
   const long M = d.n_rows;
@@ -1491,41 +1495,64 @@ __global__ void diag_ess_kernel(const DiagParams d) {
   auto x = [&](int c, long i) {
     return d.samples[((size_t)c * d.n_cols + col) * M + i];
   };
-  __shared__ double mu[32];
   if (lane < C) {
     double s = 0.0;
     for (long i = 0; i < M; ++i) s += x(lane, i);
     mu[lane] = s / (double)M;
   }
   __syncwarp();
-  for (long t = lane; t < M; t += 32) {
+  // avg_autocov(t), P:src/diagnostics.cpp: chains in order, biased 1/M
+  auto autocov = [&](long t) {
     double total = 0.0;
     for (int c = 0; c < C; ++c) {
       double s = 0.0;
       for (long i = 0; i + t < M; ++i) s += (x(c, i) - mu[c]) * (x(c, i + t) - mu[c]);
       total += s / (double)M;
     }
-    lagc[t] = total / (double)C;
+    return total / (double)C;
+  };
+  double c0 = 0.0, tau = 0.0, prev = INFINITY;
+  int status = -1;  // lane 0: -1 running, 0 ok (scan ended), 2 degenerate
+  for (long base = 0; base < M; base += 64) {
+    for (int j = lane; j < 64; j += 32) {
+      const long t = base + j;
+      lagb[j] = t < M ? autocov(t) : 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (base == 0) {
+        c0 = lagb[0];
+        if (!(c0 > 0.0)) status = 2;
+      }
+      for (int j = 0; status < 0 && j < 64; j += 2) {
+        const long k2 = base + j;  // 2k
+        if (!(k2 + 1 < M)) {
+          status = 0;
+          break;
+        }
+        const double re = lagb[j] / c0;
+        const double ro = lagb[j + 1] / c0;
+        double pair = re + ro;
+        if (pair <= 0.0) {
+          status = 0;
+          break;
+        }
+        pair = (prev < pair) ? prev : pair;  // std::min(pair, prev)
+        prev = pair;
+        tau += pair;
+      }
+    }
+    const int st = __shfl_sync(0xffffffffu, status, 0);
+    __syncwarp();
+    if (st >= 0) break;
   }
-  __syncwarp();
   if (lane != 0) return;
-  const double c0 = lagc[0];
-  if (!(c0 > 0.0)) {
+  if (status == 2) {
     d.ess[col] = 0.0;
     d.ess_status[col] = 2;
     return;
   }
   const double total = (double)C * (double)M;
-  double tau = 0.0, prev = INFINITY;
-  for (long k = 0; 2 * k + 1 < M; ++k) {
-    const double re = lagc[2 * k] / c0;
-    const double ro = lagc[2 * k + 1] / c0;
-    double pair = re + ro;
-    if (pair <= 0.0) break;
-    pair = (prev < pair) ? prev : pair;  // std::min(pair, prev)
-    prev = pair;
-    tau += pair;
-  }
   tau = 2.0 * tau - 1.0;
   if (tau < 1.0) tau = 1.0;
   d.ess[col] = total / tau;
@@ -1539,13 +1566,7 @@ cudaError_t launch_diagnostics(const DiagParams& d, cudaStream_t s) {
   diag_rows_kernel<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(d);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || d.n_cols == 0) return e;
-  const size_t smem = sizeof(double) * (size_t)(d.n_rows > 0 ? d.n_rows : 1);
-  if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(diag_ess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  diag_ess_kernel<<<(unsigned)d.n_cols, 32, smem, s>>>(d);
+  diag_ess_kernel<<<(unsigned)d.n_cols, 32, 0, s>>>(d);
   return cudaGetLastError();
 }
 

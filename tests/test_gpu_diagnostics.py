@@ -84,3 +84,25 @@ def test_paschold_shape_diagnostics_pipeline():
     assert np.all(d.ci_lo <= d.mean) and np.all(d.mean <= d.ci_hi)
     assert not d.degenerate.any()
     assert sum(s == "ok" for s in d.ess_status) == eng.n_cols
+
+
+@pytest.mark.usefixtures("ref")
+def test_long_thinned_run_ess_matches_reference():
+    """20,000 retained rows per column (thin 1): the ESS kernel computes lags
+    in batches and stops at the Geyer cutoff like the reference's lazy
+    avg_autocov, with the same bits."""
+    counts, X, h = heterosis(30, seed=5)
+    cfg = RunConfig(chains=2, burnin=100, iterations=20000, thin=1, seed=8, save_genes=2)
+    eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg)
+    d = eng.diagnostics()
+    ref = oracle.RefEngine(counts, X, h, cfg.to_c()).diagnostics(eng.n_cols)
+    L = 5
+    hyper = list(range(2 + 2 * L))
+    for c in hyper:
+        st = {0: "ok", 1: "undefined", 2: "degenerate"}[int(ref["ess_status"][c])]
+        assert d.ess_status[c] == st
+        if st == "ok":
+            if 2 <= c < 2 + L:
+                assert d.ess[c] == pytest.approx(ref["ess"][c], rel=1e-10)
+            else:
+                assert d.ess[c] == ref["ess"][c], c
