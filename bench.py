@@ -49,15 +49,16 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-xi", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     return ap.parse_args()
 
 
-def problem(G):
+def problem(G, N=N_SAMPLES):
     from paper_1606_06659_b200 import SimSpec, builtin_design, generate
-    X = builtin_design("heterosis16x5", N_SAMPLES)
-    counts = generate(SimSpec(G=G, N=N_SAMPLES, X=X, nu=8.0, tau=0.7, theta=THETA,
+    X = builtin_design("heterosis16x5", N)
+    counts = generate(SimSpec(G=G, N=N, X=X, nu=8.0, tau=0.7, theta=THETA,
                               sigma=SIGMA, seed=1)).counts
-    return counts, X, np.zeros(N_SAMPLES)
+    return counts, X, np.zeros(N)
 
 
 def bytes_per_gene_iter(N, L, n_gene_contrasts):
@@ -334,6 +335,36 @@ def run_b200(a, rank, world, local_rank):
                             "(gene, column); t with k = 3; same data, chains, burn-in and "
                             "device timing as value; extension, not in the reference")
 
+    # BASELINE configs 4 and 5 on this GPU (parity cases, not the headline):
+    # same chains and device timing, 100 burn-in sweeps, 20 timed
+    other = None
+    if not dist and not a.no_other_configs:
+        other = {}
+        for name, Gx, Nx in (("G1000000_N16", 1_000_000, 16), ("G200000_N64", 200_000, 64)):
+            cx, Xx, hx_ = problem(Gx, Nx)
+            ex = GibbsEngine(CountMatrix(cx), ModelSpec(Xx, hx_),
+                             RunConfig(chains=C, burnin=100, iterations=40, thin=20, seed=7,
+                                       save_genes=20),
+                             contrasts=[heterosis_contrast()], device=local_rank)
+            lx, hdx = ex._lib, ex.handle
+            ok(lx.cmc_engine_begin(hdx, byref(err)))
+            ok(lx.cmc_engine_sweeps(hdx, 1, 106, byref(err)))
+            ok(lx.cmc_engine_sync(hdx, byref(err)))
+            sx = torch.cuda.ExternalStream(lx.cmc_engine_stream(hdx))
+            y0, y1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            y0.record(sx)
+            ok(lx.cmc_engine_sweeps(hdx, 106, 126, byref(err)))
+            y1.record(sx)
+            ok(lx.cmc_engine_sync(hdx, byref(err)))
+            torch.cuda.synchronize()
+            yms = y0.elapsed_time(y1) / 20
+            other[name] = {"value": C * Gx / (yms * 1e-3), "ms_per_step": yms, "chains": C}
+            del ex, cx
+        other["note"] = ("BASELINE configs 4 (G=1M, N=16; one GPU) and 5 (G=200k, N=64), "
+                         "heterosis16x5, normal prior, 100 burn-in then 20 device-timed "
+                         "monitored sweeps")
+
     # end to end through the public API from host arrays: create (H2D of
     # counts + initial states), run() (burn-in + iterations), all outputs D2H
     E, BE = a.e2e_iterations, a.e2e_burnin
@@ -407,6 +438,7 @@ def run_b200(a, rank, world, local_rank):
         "clocks": clk,
         "burnin": burnin,
         "xi_priors": xi_rates,
+        "other_configs": other,
         "e2e": e2e,
         "roofline": roofline,
         "cpu_baseline": cpu,
