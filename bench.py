@@ -286,6 +286,22 @@ def run_b200(a, rank, world, local_rank):
             tj = json.load(open(tpath))
             if tj.get("chains") == C and tj.get("G") == G:
                 traffic = tj.get("dram_bytes_per_launch")
+        # the bound the sweep actually sits on: warp-instruction issue
+        # (profiles/sweep_instructions.json: ncu count per 4-chain sweep)
+        issue = None
+        ipath = os.path.join(ROOT, "profiles", "sweep_instructions.json")
+        if os.path.exists(ipath):
+            ij = json.load(open(ipath))
+            if ij.get("chains") == C and ij.get("G") == G:
+                mhz = (clk or {}).get("sm_mhz") or 1965.0
+                ipeak = 148 * 4 * mhz * 1e6          # 1 warp-instruction / scheduler / clock
+                iach = ij["warp_inst_per_sweep"] / (ms / K * 1e-3)
+                issue = {"bound": "issue", "achieved": iach, "peak": ipeak,
+                         "unit": "warp-inst/s", "frac": iach / ipeak,
+                         "warp_inst_per_sweep": ij["warp_inst_per_sweep"],
+                         "note": "ncu instruction count of eps+gene+leaf kernels per 4-chain "
+                                 "sweep over the live ms_per_step; peak = 148 SMs x 4 "
+                                 "schedulers x SM clock"}
         roofline = {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
@@ -295,9 +311,10 @@ def run_b200(a, rank, world, local_rank):
             "kernel_ms": gene_ms.value, "tail_ms": tail_ms.value,
             "kernel_share_of_step": gene_ms.value / (gene_ms.value + tail_ms.value),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
-            "note": "the sweep is FP64/INT64-latency bound, not HBM bound: see DESIGN.md "
-                    "'Roofline' for the measured FP64 (36.3 TFLOP/s DFMA, 8.1e11 exp/s) "
-                    "and Philox (1.1e11 blocks/s) denominators",
+            "note": "the sweep is issue/latency bound, not HBM bound (see issue_roofline "
+                    "and DESIGN.md 'Roofline': measured FP64 36.3 TFLOP/s DFMA, 8.1e11 exp/s, "
+                    "Philox 1.1e11 blocks/s)",
+            "issue_roofline": issue,
         }
     del eng
     torch.cuda.synchronize()
