@@ -23,6 +23,7 @@ constexpr int kGeneBlock = 128;   // threads (= genes) per eps / xi block
 #define CMC_GENE_THREADS 128
 #endif
 constexpr int kGeneThreads = CMC_GENE_THREADS;  // threads (= genes) per gene block
+constexpr int kTailWarps = 16;    // warps per leaf/hyper block (512 threads)
 constexpr int kMaxContrasts = 8;
 constexpr int kMaxTerms = 32;
 constexpr int kMaxCoefs = 64;

@@ -906,17 +906,9 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
   const int L = p.L, Q = leaf_q_a(L, p.xi_any);
   const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   const double Gd = (double)p.G_total;
-  if constexpr (!XI) {
-    (void)nwarps;
-    if (warp < Q) {
-      const double r = warp_pairwise_leaves(part_view(p.partA, p, slot, Q), warp, p.n_leaves_total);
-      if ((tid & 31) == 0) red[warp] = r;
-    }
-  } else {  // Q = 2 + 2L may exceed the block's 32 warps
-    for (int q = warp; q < Q; q += nwarps) {
-      const double r = warp_pairwise_leaves(part_view(p.partA, p, slot, Q), q, p.n_leaves_total);
-      if ((tid & 31) == 0) red[q] = r;
-    }
+  for (int q = warp; q < Q; q += nwarps) {  // Q may exceed the block's warps
+    const double r = warp_pairwise_leaves(part_view(p.partA, p, slot, Q), q, p.n_leaves_total);
+    if ((tid & 31) == 0) red[q] = r;
   }
   __syncthreads();
   if (tid == 0) {
@@ -1072,8 +1064,11 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned total
 
 // Leaf sums of log gamma (q=0), 1/gamma (q=1), beta_l (q=2+l); one warp
 // per quantity, one block per local leaf.
+// Tail kernels run at most kTailWarps warps per block (registers for 512
+// threads are guaranteed); warps loop over the 2 + L (+ L) quantities.
 template <bool XI>
-__global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
+__global__ void __launch_bounds__(32 * kTailWarps) leaf_a_kernel(const SweepParams p,
+                                                                 const long m_off) {
   WarpTrace wt(p, 3, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
@@ -1087,12 +1082,12 @@ __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
   const long lpr = p.leaves_per_rank;
   const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
   if constexpr (!XI) {
-    if (warp < Q) {
-      const double* src = warp == 0   ? p.log_gam + so * G
-                          : warp == 1 ? p.inv_gam + so * G
-                                      : p.beta + so * L * G + (size_t)(warp - 2) * G;
+    for (int q = warp; q < Q; q += nwarps) {
+      const double* src = q == 0   ? p.log_gam + so * G
+                          : q == 1 ? p.inv_gam + so * G
+                                   : p.beta + so * L * G + (size_t)(q - 2) * G;
       const double s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
-      if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Q + warp) * lpr + lb] = s;
+      if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Q + q) * lpr + lb] = s;
     }
   } else {
     // xi engine: quantities [log gamma, 1/gamma, S_l, W_l] (sweep.h), looped
@@ -1123,7 +1118,8 @@ __global__ void leaf_a_kernel(const SweepParams p, const long m_off) {
 }
 
 template <bool XI>
-__global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
+__global__ void __launch_bounds__(32 * kTailWarps) hyper_a_kernel(const SweepParams p,
+                                                                  const long m_off) {
   const int slot = p.slot_base + blockIdx.x;
   if (stalled_chain(p.hyper + slot)) return;
   hyper_a_body<XI>(p, slot, *p.d_m + m_off);
@@ -1131,7 +1127,8 @@ __global__ void hyper_a_kernel(const SweepParams p, const long m_off) {
 
 // Leaf sums of (beta_l - theta_l)^2 with theta of this iteration.
 template <bool XI>
-__global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
+__global__ void __launch_bounds__(32 * kTailWarps) leaf_b_kernel(const SweepParams p,
+                                                                 const long m_off) {
   WarpTrace wt(p, 4, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
@@ -1142,12 +1139,12 @@ __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
   const long lb = blockIdx.x;
   const long start = lb * kLeaf;
   const long end = min((long)G, start + kLeaf);
-  if (warp < L) {
-    const double th = hp->theta[warp];
-    const double* src = p.beta + so * L * G + (size_t)warp * G;
+  for (int q = warp; q < L; q += blockDim.x >> 5) {
+    const double th = hp->theta[q];
+    const double* src = p.beta + so * L * G + (size_t)q * G;
     double s;
-    if (XI && p.xi_fam[warp] != CMC_PRIOR_NORMAL) {  // extension: /xi
-      const double* xs = p.xi + so * L * G + (size_t)warp * G;
+    if (XI && p.xi_fam[q] != CMC_PRIOR_NORMAL) {  // extension: /xi
+      const double* xs = p.xi + so * L * G + (size_t)q * G;
       s = warp_leaf_sum(
           [&](long i) {
             const double dl = src[i] - th;
@@ -1165,7 +1162,7 @@ __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
     if (lane == 0) {
       const long lpr = p.leaves_per_rank;
       const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
-      p.partB[((rank * p.C + (slot - p.slot_base)) * L + warp) * lpr + lb] = s;
+      p.partB[((rank * p.C + (slot - p.slot_base)) * L + q) * lpr + lb] = s;
     }
   }
   if (!p.fuse_tail) return;
@@ -1173,7 +1170,8 @@ __global__ void leaf_b_kernel(const SweepParams p, const long m_off) {
   hyper_b_body(p, slot, *p.d_m + m_off);
 }
 
-__global__ void hyper_b_kernel(const SweepParams p, const long m_off) {
+__global__ void __launch_bounds__(32 * kTailWarps) hyper_b_kernel(const SweepParams p,
+                                                                  const long m_off) {
   const int slot = p.slot_base + blockIdx.x;
   if (stalled_chain(p.hyper + slot)) return;
   hyper_b_body(p, slot, *p.d_m + m_off);
@@ -1331,7 +1329,7 @@ cudaError_t launch_xi_sweep(const SweepParams& p, int chains, long m_off,
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
                           cudaStream_t s) {
   const int Q = leaf_q_a(p.L, p.xi_any);
-  const int threads = 32 * (Q < 32 ? Q : 32);
+  const int threads = 32 * (Q < kTailWarps ? Q : kTailWarps);
   dim3 grid((unsigned)p.n_leaves_local, (unsigned)chains);
   if (p.xi_any)
     return launch_prio(leaf_a_kernel<true>, grid, dim3(threads < 64 ? 64 : threads), 0, s,
@@ -1343,11 +1341,12 @@ cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,
 cudaError_t launch_hyper_a(const SweepParams& p, int chains, long m_off,
                            cudaStream_t s) {
   const int Q = leaf_q_a(p.L, p.xi_any);
+  const int threads = 32 * (Q < kTailWarps ? Q : kTailWarps);
   if (p.xi_any)
-    return launch_prio(hyper_a_kernel<true>, dim3(chains), dim3(32 * (Q < 32 ? Q : 32)), 0, s,
+    return launch_prio(hyper_a_kernel<true>, dim3(chains), dim3(threads < 64 ? 64 : threads), 0, s,
                        p.prio_tail, p, m_off);
-  return launch_prio(hyper_a_kernel<false>, dim3(chains), dim3(32 * (Q < 32 ? Q : 32)), 0, s,
-                     p.prio_tail, p, m_off);
+  return launch_prio(hyper_a_kernel<false>, dim3(chains), dim3(threads < 64 ? 64 : threads), 0,
+                     s, p.prio_tail, p, m_off);
 }
 
 cudaError_t launch_leaf_b(const SweepParams& p, int chains, long m_off,

@@ -1,0 +1,109 @@
+"""GPU: edge shapes the heterosis bench never reaches, each bit-for-bit
+against the oracle (θ to 1e-12), the way the reference's own tests probe
+them (P:tests/test_engine.cpp, test_model.cpp clamp semantics):
+
+* continuous covariates: up to N distinct values per model-matrix column,
+  so the generic gene kernel (group sums in shared memory) runs;
+* L = 16, the widest model matrix this build supports;
+* the exp(700) clamp: offsets push h + xb + ε past 700, and the clamp
+  counts must agree too;
+* ragged G (not a multiple of the 128-gene block or the 1024-gene leaf)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1606_06659_b200 import _abi
+
+from helpers import Product, advance, mismatch, packed_start
+
+pytestmark = pytest.mark.gpu
+
+
+def _sim(G, X, h, seed):
+    from paper_1606_06659_b200 import SimSpec, generate
+    L = X.shape[1]
+    rng = np.random.default_rng(seed)
+    theta = np.concatenate([[2.0], rng.normal(0, 0.2, L - 1)])
+    sigma = np.full(L, 0.3)
+    return generate(SimSpec(G=G, N=X.shape[0], X=X, h=h, nu=8.0, tau=0.7, theta=list(theta),
+                            sigma=list(sigma), seed=seed)).counts
+
+
+def _pair_sweeps(counts, X, h, cfg, sweeps, start=1, chain=0):
+    orc = oracle.OracleEngine(counts, X, h, cfg)
+    gpu = Product(counts, X, h, cfg)
+    st, tw, ta = packed_start(orc, chain, cfg.w_init)
+    if start > 1:
+        advance(orc, st, tw, ta, chain, 1, start)
+    g = [st.copy(), tw.copy(), ta.copy()]
+    G, N = counts.shape
+    L = X.shape[1]
+    th0 = G * N + G + G * L
+    clamps = 0
+    for m in range(start, start + sweeps):
+        c1 = orc.iterate(st, tw, ta, chain, m)
+        c2 = gpu.iterate(*g, chain, m)
+        assert c1 == c2, f"clamps m={m}: {c1} vs {c2}"
+        clamps += c1
+        bad = [i for i in mismatch(g[0], st) if not th0 <= i < th0 + L]
+        assert not bad, f"m={m}: {bad[:8]}"
+        np.testing.assert_allclose(g[0][th0:th0 + L], st[th0:th0 + L], rtol=1e-12, atol=0)
+        assert not len(mismatch(g[1], tw)) and not len(mismatch(g[2], ta))
+    return clamps
+
+
+def test_continuous_covariates_generic_group_path():
+    rng = np.random.default_rng(3)
+    N = 12
+    X = np.column_stack([np.ones(N), rng.normal(size=N), rng.uniform(-1, 1, size=N)])
+    h = rng.normal(0, 0.1, size=N)
+    counts = _sim(700, X, h, 3)
+    cfg = _abi.make_config(chains=1, burnin=30, iterations=30, thin=10, seed=4, save_genes=5)
+    _pair_sweeps(counts, X, h, cfg, 6)
+    _pair_sweeps(counts, X, h, cfg, 3, start=25)
+
+
+def test_widest_model_matrix():
+    rng = np.random.default_rng(5)
+    N, L = 24, 16
+    X = np.column_stack([np.ones(N), rng.choice([-1.0, 0.0, 1.0], size=(N, L - 1))])
+    assert np.linalg.matrix_rank(X) == L
+    counts = _sim(300, X, np.zeros(N), 5)
+    cfg = _abi.make_config(chains=1, burnin=20, iterations=20, thin=10, seed=6, save_genes=3)
+    _pair_sweeps(counts, X, np.zeros(N), cfg, 5)
+
+
+def test_exp_clamp_path_counts_agree():
+    """A first slice interval of width 1000 (w_init) puts step-out bounds and
+    shrink proposals past h + xb + eps = 700, where clamped_exp returns
+    exp(700) and bumps the ClampCounter (P:src/model.cpp:13-19); the device's
+    counts equal the oracle's sweep by sweep.  (Offsets near 700 instead make
+    every density ~1e303, which absorbs log(u) and stalls the reference too.)"""
+    from paper_1606_06659_b200 import builtin_design
+    X = builtin_design("heterosis16x5", 16)
+    counts = _sim(500, X, np.zeros(16), 7)
+    cfg = _abi.make_config(chains=1, burnin=20, iterations=20, thin=10, seed=8, save_genes=3,
+                           w_init=1000.0)
+    clamps = _pair_sweeps(counts, X, np.zeros(16), cfg, 4)
+    assert clamps > 0
+
+
+@pytest.mark.parametrize("G", [1, 127, 129, 1023, 1025, 2049])
+def test_ragged_gene_counts_run(G):
+    """run() with batched chains at block/leaf boundaries: every chain equals
+    the oracle's run_chain."""
+    from paper_1606_06659_b200 import builtin_design
+    X = builtin_design("heterosis16x5", 16)
+    counts = _sim(G, X, np.zeros(16), 11)
+    cfg = _abi.make_config(chains=2, burnin=20, iterations=20, thin=5, seed=9,
+                           save_genes=min(4, G))
+    outs = Product(counts, X, np.zeros(16), cfg).run()
+    N, L = 16, 5
+    th0 = G * N + G + G * L
+    for c in range(2):
+        o = oracle.OracleEngine(counts, X, np.zeros(16), cfg).run_chain(c)
+        bad = [i for i in mismatch(outs[c]["final"], o["final"]) if not th0 <= i < th0 + L]
+        assert not bad, (G, c, bad[:5])
+        for k in ("mean", "meansq"):
+            badk = [i for i in mismatch(outs[c][k], o[k]) if not 2 <= i < 2 + L]
+            assert not badk, (G, c, k, badk[:5])
