@@ -107,3 +107,67 @@ def test_ragged_gene_counts_run(G):
         for k in ("mean", "meansq"):
             badk = [i for i in mismatch(outs[c][k], o[k]) if not 2 <= i < 2 + L]
             assert not badk, (G, c, k, badk[:5])
+
+
+def _run_vs_oracle(counts, X, h, cfg, contrasts=(), priors=None, chains=None):
+    outs = Product(counts, X, h, cfg, contrasts=list(contrasts), priors=priors).run()
+    G, N = counts.shape
+    L = X.shape[1]
+    th0 = G * N + G + G * L
+    orc = oracle.OracleEngine(counts, X, h, cfg, contrasts=list(contrasts), priors=priors)
+    for c in range(chains or cfg.chains):
+        o = orc.run_chain(c)
+        bad = [i for i in mismatch(outs[c]["final"], o["final"]) if not th0 <= i < th0 + L]
+        assert not bad, (c, bad[:5])
+        for k in ("mean", "meansq"):
+            badk = [i for i in mismatch(outs[c][k], o[k]) if not 2 <= i < 2 + L]
+            assert not badk, (c, k, badk[:5])
+        assert not len(mismatch(outs[c]["prob"], o["prob"])), c
+    return outs
+
+
+def test_xi_priors_widest_matrix_and_generic_groups():
+    rng = np.random.default_rng(21)
+    N, L = 24, 16
+    X = np.column_stack([np.ones(N), rng.normal(size=(N, L - 1))])   # continuous: J = N
+    counts = _sim(200, X, np.zeros(N), 21)
+    pri = {"beta_prior": ["normal", "laplace", "t", "horseshoe"] * 4, "t_df": 4.0}
+    cfg = _abi.make_config(chains=2, burnin=10, iterations=10, thin=5, seed=2, save_genes=2)
+    _run_vs_oracle(counts, X, np.zeros(N), cfg, priors=pri)
+
+
+def test_eight_contrasts_every_scope():
+    from paper_1606_06659_b200 import builtin_design
+    X = builtin_design("heterosis16x5", 16)
+    counts = _sim(300, X, np.zeros(16), 23)
+    cons = [
+        [([("beta_col", 1, 2.0), ("beta_col", 3, 1.0)], 0.0),
+         ([("beta_col", 2, 2.0), ("beta_col", 3, 1.0)], 0.0)],
+        [([("beta_col", 1, 1.0)], 0.1)],
+        [([("gamma", 0, 1.0)], 0.5)],
+        [([("theta", 1, 1.0), ("sigma", 0, -1.0)], 0.0)],
+        [([("nu", 0, 1.0)], 5.0)],
+        [([("tau", 0, 1.0)], 0.5), ([("sigma", 2, 1.0)], 0.1)],
+        [([("beta_col", 4, 1.0), ("gamma", 0, -0.1)], -0.2)],
+        [([("beta_col", 0, 1.0), ("theta", 0, -1.0)], 0.0)],
+    ]
+    cfg = _abi.make_config(chains=2, burnin=20, iterations=30, thin=10, seed=4, save_genes=3)
+    _run_vs_oracle(counts, X, np.zeros(16), cfg, contrasts=cons)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(G=1, chains=4, save_genes=20),              # one gene, both lanes, save > G
+    dict(G=60, chains=2, thin=50, iterations=20),    # thin > iterations: no sample rows
+    dict(G=60, chains=2, burnin=1),                  # tune_cutoff resolves to 0
+    dict(G=200, chains=8),                           # lanes of 4 chains
+])
+def test_run_configuration_corners(kw):
+    from paper_1606_06659_b200 import builtin_design
+    G = kw.pop("G")
+    X = builtin_design("heterosis16x5", 16)
+    counts = _sim(G, X, np.zeros(16), 29)
+    args = dict(chains=2, burnin=20, iterations=20, thin=5, seed=6, save_genes=4)
+    args.update(kw)
+    cfg = _abi.make_config(**args)
+    _run_vs_oracle(counts, X, np.zeros(16), cfg,
+                   contrasts=[[([("beta_col", 1, 1.0)], 0.0)]])
