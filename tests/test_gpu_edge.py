@@ -171,3 +171,40 @@ def test_run_configuration_corners(kw):
     cfg = _abi.make_config(**args)
     _run_vs_oracle(counts, X, np.zeros(16), cfg,
                    contrasts=[[([("beta_col", 1, 1.0)], 0.0)]])
+
+
+def test_conjugate_direct_with_xi_prior():
+    """gamma/tau by direct draws (1e-12, Marsaglia-Tsang through pow/log) with
+    a Laplace xi column; everything slice-sampled stays bit-identical."""
+    from paper_1606_06659_b200 import builtin_design
+    X = builtin_design("heterosis16x5", 16)
+    counts = _sim(300, X, np.zeros(16), 31)
+    cfg = _abi.make_config(chains=1, burnin=20, iterations=20, thin=10, seed=3,
+                           sampler_mode=_abi.CMC_CONJUGATE_DIRECT)
+    pri = {"beta_prior": ["normal", "laplace", "normal", "normal", "normal"]}
+    orc = oracle.OracleEngine(counts, X, np.zeros(16), cfg, priors=pri)
+    gpu = Product(counts, X, np.zeros(16), cfg, priors=pri)
+    st, tw, ta = packed_start(orc, 0)
+    g = [st.copy(), tw.copy(), ta.copy()]
+    for m in range(1, 5):
+        orc.iterate(st, tw, ta, 0, m)
+        gpu.iterate(*g, 0, m)
+    np.testing.assert_allclose(g[0], st, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.usefixtures("ref")
+def test_diagnostics_at_the_chain_limit():
+    """32 chains (the device diagnostics' limit) against the reference's
+    build_diagnostics numerics."""
+    from paper_1606_06659_b200 import CountMatrix, GibbsEngine, ModelSpec, RunConfig, builtin_design
+    X = builtin_design("heterosis16x5", 16)
+    counts = _sim(40, X, np.zeros(16), 33)
+    cfg = RunConfig(chains=32, burnin=20, iterations=20, thin=5, seed=5, save_genes=2)
+    eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, np.zeros(16)), cfg)
+    d = eng.diagnostics()
+    ref = oracle.RefEngine(counts, X, np.zeros(16), cfg.to_c()).diagnostics(eng.n_cols)
+    L = 5
+    keep = np.ones(len(d.rhat), bool)
+    keep[2:2 + L] = False
+    assert not len(mismatch(d.rhat[keep], ref["rhat"][keep]))
+    assert not len(mismatch(d.mean[keep], ref["mean"][keep]))
