@@ -89,3 +89,62 @@ def test_sharded_leaf_exchange_is_bit_exact(G):
     r1, f1, t1 = out[1]
     assert r0 == r1 == f0 == f1, "sharded reduction differs from det_transform_sum"
     assert t0 == t1, "replicated hyper draw differs across ranks"
+
+
+def lane_worker(rank, world, port, G, C, Q, lanes, out):
+    """The two-lane layout of the sharded engine (engine.cu
+    enqueue_sweep_on): lane k owns chains [slot0, slot0 + n) and the section
+    [rank][n][Q][lpr] at offset world * slot0 * Q * lpr of the partial
+    buffer, indexed by the lane-relative chain (sweep_kernels.cu PartView);
+    each lane all-gathers its own section on its own communicator."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    groups = [dist.new_group(list(range(world))) for _ in lanes]  # ncclCommSplit per lane
+    import oracle
+    from paper_1606_06659_b200 import _abi
+    lib = _abi.load_library()
+    orc = oracle.load_oracle()
+    rng = np.random.default_rng(321)
+    data = rng.standard_normal((C, Q, G))
+    lo, hi = c_long(), c_long()
+    lib.cmc_shard_bounds(G, rank, world, byref(lo), byref(hi))
+    n_leaves = (G + LEAF - 1) // LEAF
+    lpr = (n_leaves + world - 1) // world
+    buf = torch.zeros(world * C * Q * lpr, dtype=torch.float64)
+    res = np.zeros((C, Q))
+    for k, (slot0, n) in enumerate(lanes):
+        base = world * slot0 * Q * lpr
+        for c in range(n):
+            for q in range(Q):
+                for g0 in range(lo.value, hi.value, LEAF):
+                    leaf = g0 // LEAF
+                    buf[base + ((rank * n + c) * Q + q) * lpr + leaf % lpr] = \
+                        serial_sum(data[slot0 + c, q, g0:min(G, g0 + LEAF)])
+        cnt = n * Q * lpr
+        sec = buf[base:base + world * cnt]
+        mine = sec[rank * cnt:(rank + 1) * cnt].clone()
+        dist.all_gather_into_tensor(sec, mine, group=groups[k])
+        buf[base:base + world * cnt] = sec
+        for c in range(n):
+            for q in range(Q):
+                leaves = np.array([buf[base + ((L // lpr * n + c) * Q + q) * lpr + L % lpr].item()
+                                   for L in range(n_leaves)])
+                res[slot0 + c, q] = orc.orc_pairwise_sum(
+                    leaves.ctypes.data_as(POINTER(c_double)), n_leaves)
+    full = np.array([[orc.orc_det_sum(np.ascontiguousarray(data[c, q]).ctypes.data_as(
+        POINTER(c_double)), G) for q in range(Q)] for c in range(C)])
+    out[rank] = (res.tobytes(), full.tobytes())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G", [5000, 2100])
+def test_two_lane_sections_are_bit_exact(G):
+    world, C, Q = 2, 4, 3
+    lanes = [(0, 2), (2, 2)]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(lane_worker, args=(world, free_port(), G, C, Q, lanes, out), nprocs=world, join=True)
+    r0, f0 = out[0]
+    r1, f1 = out[1]
+    assert r0 == r1 == f0 == f1, "per-lane sharded reduction differs from det_transform_sum"
