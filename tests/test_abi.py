@@ -2,7 +2,6 @@
 header declares, and its host-side logic (validation, configuration
 resolution, saved-gene selection, initial states, shard bounds, synthetic
 data) matches the oracle.  No sweep runs here (that needs the device)."""
-import ctypes
 import os
 import re
 from ctypes import byref, c_long

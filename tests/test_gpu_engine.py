@@ -3,15 +3,13 @@ behaviours P:tests/test_engine.cpp pins, through the mirrored public API
 (paper_1606_06659_b200.GibbsEngine).  Slice-sampled values are compared bit
 for bit; theta (AS241 tail through log) and conjugate-direct draws within
 REL_TOL = 1e-12 (north_star single-sweep tolerance)."""
-import os
-
 import numpy as np
 import pytest
 
 import oracle
-from paper_1606_06659_b200 import (ChainState, ConfigError, CountMatrix, GibbsEngine,
-                                   ModelSpec, RunConfig, SamplerStallError, SliceConfig,
-                                   TuningState, _abi, builtin_design, heterosis_contrast)
+from paper_1606_06659_b200 import (CountMatrix, GibbsEngine, ModelSpec, RunConfig,
+                                   SamplerStallError, SliceConfig, TuningState, _abi,
+                                   heterosis_contrast)
 from paper_1606_06659_b200._abi import sizes
 
 from helpers import HETEROSIS, Product, heterosis, mismatch, simulated, tiny

@@ -9,10 +9,8 @@ log.  run_report.json matches key for key; the float layout
 is checked against the reference's nlohmann output on wall_seconds."""
 import csv
 import json
-import os
 import re
 
-import numpy as np
 import pytest
 
 import oracle
