@@ -326,37 +326,42 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(e->saved_slot.alloc(slot.size()));
   CUDA_TRY(cudaMemcpy(e->saved_slot.p, slot.data(), sizeof(int) * slot.size(),
                       cudaMemcpyHostToDevice));
-  // chain state
+  // chain state: slots 0..C-1 are run()'s chains; slot C is iterate()'s
+  // scratch (the reference's iterate works on caller-owned state, so it must
+  // not disturb a run).  Accumulators exist for run chains only: iterate()
+  // sweeps with the monitors off.
+  const long Cs = C + 1;
   const size_t gn = (size_t)G * N * C, gl = (size_t)G * L * C, gc = (size_t)G * C;
-  CUDA_TRY(e->eps.alloc(gn));
-  CUDA_TRY(e->eps_w.alloc(gn));
-  CUDA_TRY(e->eps_wa.alloc(gn));
-  CUDA_TRY(e->gam.alloc(gc));
-  CUDA_TRY(e->gam_w.alloc(gc));
-  CUDA_TRY(e->gam_wa.alloc(gc));
-  CUDA_TRY(e->beta.alloc(gl));
-  CUDA_TRY(e->beta_w.alloc(gl));
-  CUDA_TRY(e->beta_wa.alloc(gl));
-  CUDA_TRY(e->log_gam.alloc(gc));
-  CUDA_TRY(e->inv_gam.alloc(gc));
+  const size_t sn = (size_t)G * N * Cs, sl = (size_t)G * L * Cs, sc = (size_t)G * Cs;
+  CUDA_TRY(e->eps.alloc(sn));
+  CUDA_TRY(e->eps_w.alloc(sn));
+  CUDA_TRY(e->eps_wa.alloc(sn));
+  CUDA_TRY(e->gam.alloc(sc));
+  CUDA_TRY(e->gam_w.alloc(sc));
+  CUDA_TRY(e->gam_wa.alloc(sc));
+  CUDA_TRY(e->beta.alloc(sl));
+  CUDA_TRY(e->beta_w.alloc(sl));
+  CUDA_TRY(e->beta_wa.alloc(sl));
+  CUDA_TRY(e->log_gam.alloc(sc));
+  CUDA_TRY(e->inv_gam.alloc(sc));
   CUDA_TRY(e->acc_eps.alloc(4 * gn));
   CUDA_TRY(e->acc_gam.alloc(4 * gc));
   CUDA_TRY(e->acc_beta.alloc(4 * gl));
   if (e->xi_any) {
-    CUDA_TRY(e->xi.alloc(gl));
-    CUDA_TRY(e->xi_w.alloc(gl));
-    CUDA_TRY(e->xi_wa.alloc(gl));
+    CUDA_TRY(e->xi.alloc(sl));
+    CUDA_TRY(e->xi_w.alloc(sl));
+    CUDA_TRY(e->xi_wa.alloc(sl));
     CUDA_TRY(e->acc_xi.alloc(4 * gl));
   }
   CUDA_TRY(e->cprob.alloc(std::max<long>(1, prob_len(e)) * C));
   CUDA_TRY(e->samples.alloc(std::max<long>(1, e->n_cols * e->n_rows) * C));
-  CUDA_TRY(e->hyper.alloc((size_t)C));
-  CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * C));
+  CUDA_TRY(e->hyper.alloc((size_t)Cs));
+  CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * Cs));
   CUDA_TRY(e->xfer.alloc((size_t)std::max(N, L) * G));
   const long n_leaves_total = (e->G_total + kLeaf - 1) / kLeaf;
   const long lpr = (n_leaves_total + e->world - 1) / e->world;
-  CUDA_TRY(e->partA.alloc((size_t)e->world * C * Q * lpr));
-  CUDA_TRY(e->partB.alloc((size_t)e->world * C * L * lpr));
+  CUDA_TRY(e->partA.alloc((size_t)e->world * Cs * Q * lpr));
+  CUDA_TRY(e->partB.alloc((size_t)e->world * Cs * L * lpr));
   CUDA_TRY(e->dctab.alloc(1));
   CUDA_TRY(cudaMemcpy(e->dctab.p, &e->ctab, sizeof(ContrastTable),
                       cudaMemcpyHostToDevice));
@@ -1157,9 +1162,10 @@ int cmc_engine_set_state(cmc_engine* e, long chain, const double* state,
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
-  // the reference's iterate() takes any chain id: state lives in slot
-  // chain mod C, the chain id only keys the random stream
-  return upload_state(e, chain % e->C, state, tw, ta, err);
+  // the reference's iterate() takes any chain id and caller-owned state:
+  // the state lives in the scratch slot C (a run()'s chains stay untouched),
+  // the chain id only keys the random stream
+  return upload_state(e, e->C, state, tw, ta, err);
 }
 
 int cmc_engine_get_state(cmc_engine* e, long chain, double* state, double* tw,
@@ -1172,7 +1178,7 @@ int cmc_engine_get_state(cmc_engine* e, long chain, double* state, double* tw,
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(e->device));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
-  return download_state(e, chain % e->C, state, tw, ta, err);
+  return download_state(e, e->C, state, tw, ta, err);
 }
 
 int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
@@ -1184,8 +1190,9 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
   int rc = ensure_device(e, err);
   if (rc) return rc;
   CUDA_TRY(cudaSetDevice(e->device));
+  const long run_m = e->host_m;  // a run()'s iteration counter, restored below
   if ((rc = set_device_m(e, m, err))) return rc;
-  const long slot = chain % e->C;
+  const long slot = e->C;  // scratch slot: a run()'s chains stay untouched
   Hyper hp;
   CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + slot, sizeof(Hyper), cudaMemcpyDeviceToHost));
   const unsigned long long before = hp.clamps;
@@ -1204,6 +1211,7 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + slot, sizeof(Hyper), cudaMemcpyDeviceToHost));
   if (clamps) *clamps += hp.clamps - before;
+  if ((rc = set_device_m(e, run_m, err))) return rc;
   if (hp.err_key != kNoError || hp.err_key_eps != kNoError)
     return check_stall(e, slot, slot + 1, err);
   return CMC_OK;

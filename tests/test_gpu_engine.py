@@ -215,3 +215,36 @@ def test_g1m_properties():
     assert np.array_equal(a.final_state.pack(), b.final_state.pack())
     assert np.array_equal(a.beta_acc.mean, b.beta_acc.mean)
     assert a.clamp_events == b.clamp_events
+
+
+def test_iterate_after_run_leaves_the_run_untouched():
+    """iterate() works on caller-owned state (the reference's contract): on
+    the device it uses a scratch slot and restores the iteration counter, so
+    a finished run()'s outputs and diagnostics are unchanged by it."""
+    counts, X, h = heterosis(300, seed=2)
+    eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, h),
+                      RunConfig(chains=2, burnin=20, iterations=30, thin=10, seed=4))
+    outs = eng.run()
+    d0 = eng.diagnostics()
+    st, tu = eng.initial_state(0), eng.tuning_state()
+    for m in range(1, 4):
+        eng.iterate(st, tu, 0, m)
+    d1 = eng.diagnostics()
+    assert np.array_equal(d0.rhat, d1.rhat)
+    for c in range(2):
+        fresh = eng._output(c)
+        assert np.array_equal(fresh.final_state.pack(), outs[c].final_state.pack())
+        assert np.array_equal(fresh.beta_acc.mean, outs[c].beta_acc.mean)
+    # and the iterate sweeps equal the oracle's from the same start
+    orc = oracle.OracleEngine(counts, X, h, RunConfig(chains=2, burnin=20, iterations=30,
+                                                      thin=10, seed=4).to_c())
+    ost = orc.initial_state(0)
+    _, T, _ = sizes(300, 16, 5)
+    tw, ta = np.ones(T), np.zeros(T)
+    for m in range(1, 4):
+        orc.iterate(ost, tw, ta, 0, m)
+    th = slice(300 * 16 + 300 + 300 * 5, 300 * 16 + 300 + 300 * 5 + 5)
+    p = st.pack()
+    keep = np.ones(len(p), bool)
+    keep[th] = False
+    assert not len(mismatch(p[keep], ost[keep]))
