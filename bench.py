@@ -194,7 +194,9 @@ def run_b200(a, rank, world, local_rank):
     counts, X, h = problem(G)
     C, B, W, K = a.chains, a.burnin, a.warmup, a.steps
     prof_reps = 5
-    cfg = RunConfig(chains=C, burnin=B, iterations=W + K + prof_reps, thin=20, seed=7,
+    # iterations cover warm-up, the clock probe (below), the timed steps and
+    # the profile reps; monitors run on all of them like run_chain's
+    cfg = RunConfig(chains=C, burnin=B, iterations=W + 20000 + K + prof_reps, thin=20, seed=7,
                     save_genes=20)
     eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg,
                       contrasts=[heterosis_contrast()], device=local_rank)
@@ -227,8 +229,12 @@ def run_b200(a, rank, world, local_rank):
     b2.record(stream)
     ok(lib.cmc_engine_sweeps(hd, 1 + nb0 + nb1, B + 1, byref(err)))    # rest of burn-in
     b3.record(stream)
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0.record(stream)
     ok(lib.cmc_engine_sweeps(hd, B + 1, B + 1 + W, byref(err)))  # warm-up monitored steps
+    w1.record(stream)
     ok(lib.cmc_engine_sync(hd, byref(err)))
+    warm_ms = w0.elapsed_time(w1) / max(W, 1)
     burn_first_ms, burn_cap_ms, burn_rest_ms = (b0.elapsed_time(b1), b1.elapsed_time(b2),
                                                 b2.elapsed_time(b3))
     n_rest = B - nb0 - nb1
@@ -245,11 +251,20 @@ def run_b200(a, rank, world, local_rank):
     if dist:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    # clocks are sampled under load: untimed monitored sweeps keep the GPU busy
+    # for ~0.4 s right before the timed region, inside the sampler's window
+    n_probe = min(20000, int(400.0 / max(warm_ms, 1e-3)))
+    m0 = B + 1 + W + n_probe
     clocks = Clocks(local_rank)
     clocks.start()
-    time.sleep(0.2)
+    time.sleep(0.1)  # nvidia-smi start-up
+    ok(lib.cmc_engine_sweeps(hd, B + 1 + W, m0, byref(err)))
+    ok(lib.cmc_engine_sync(hd, byref(err)))
+    torch.cuda.synchronize()
+    if dist:
+        torch.distributed.barrier()
     e0.record(stream)
-    ok(lib.cmc_engine_sweeps(hd, B + 1 + W, B + 1 + W + K, byref(err)))
+    ok(lib.cmc_engine_sweeps(hd, m0, m0 + K, byref(err)))
     e1.record(stream)
     ok(lib.cmc_engine_sync(hd, byref(err)))
     torch.cuda.synchronize()
@@ -274,7 +289,7 @@ def run_b200(a, rank, world, local_rank):
     except Exception:
         pass
     if not dist:
-        ok(lib.cmc_engine_profile(hd, B + 1 + W + K, prof_reps, byref(gene_ms), byref(tail_ms),
+        ok(lib.cmc_engine_profile(hd, m0 + K, prof_reps, byref(gene_ms), byref(tail_ms),
                                   byref(err)))
         bpg = bytes_per_gene_iter(N_SAMPLES, 5, 1)
         per_launch = C * G * bpg
@@ -452,7 +467,9 @@ def run_b200(a, rank, world, local_rank):
                    "l2": "inputs larger than L2: ~%.0f MB touched per sweep vs 126 MB L2"
                          % (C * G * bytes_per_gene_iter(16, 5, 1) / 1e6 + G * 16 * 8 / 1e6)},
         "gpu_launches": launches,
-        "clocks": clk,
+        "clocks": dict(clk, probe_sweeps=n_probe,
+                       note="nvidia-smi -lms 50 over ~0.4 s of untimed monitored sweeps "
+                            "plus the timed region"),
         "burnin": burnin,
         "xi_priors": xi_rates,
         "other_configs": other,
