@@ -428,10 +428,13 @@ def run_b200(a, rank, world, local_rank):
            "post_burnin_only_value": C * G * E / wall,
            "note": "one GibbsEngine(...).run() with the reference's default RunConfig "
                    "(chains 4, burnin 2000, iterations 4000), host wall clock: host count "
-                   "matrix in (H2D), every sweep, all ChainOutputs out (D2H).  value counts "
-                   "every sweep the call ran (burn-in sweeps are gene-iterations too, and "
-                   "cost slightly more: tuning); post_burnin_only_value charges the whole "
-                   "wall time to the 4000 monitored sweeps"}
+                   "matrix in (H2D), every sweep, all ChainOutputs out (D2H).  An MCMC run "
+                   "has one input (the counts) and one result (the ChainOutputs), so the "
+                   "per-step byte figures are those run totals over the sweeps; a per-sweep "
+                   "host round trip would only serialise the pipeline.  value counts every "
+                   "sweep the call ran (burn-in sweeps are gene-iterations too, and cost "
+                   "slightly more: tuning); post_burnin_only_value charges the whole wall "
+                   "time to the 4000 monitored sweeps"}
     del eng2
 
     if rank != 0:
