@@ -316,6 +316,20 @@ int cmc_counts_labels(const cmc_counts* counts, int which, const char** blob,
                       size_t* bytes);
 void cmc_counts_free(cmc_counts* counts);
 
+/* The small input tables of run_fit.  cmc_model_matrix_load replaces
+ * load_model_matrix (P:src/io.cpp:178-205): rows = N samples, cols = L,
+ * data N x L row-major, names = the header's effect labels.
+ * cmc_offsets_load replaces load_offsets (P:src/io.cpp:221-243): rows = N,
+ * cols = 1, data = h.  Numbers parse as strtod over the whole cell; errors
+ * are CMC_ERR_LOAD with the reference's LoadError messages. */
+typedef struct cmc_table cmc_table;
+int cmc_model_matrix_load(const char* path, cmc_table** out, cmc_error* err);
+int cmc_offsets_load(const char* path, cmc_table** out, cmc_error* err);
+int cmc_table_dims(const cmc_table* table, long* rows, long* cols);
+const double* cmc_table_data(const cmc_table* table);
+const char* cmc_table_name(const cmc_table* table, long col);
+void cmc_table_free(cmc_table* table);
+
 /* Median-of-ratios offsets, replaces countmc::estimate_offsets
  * (P:src/model.cpp:21-68; bit-identical).  counts is G x N row-major;
  * h_out has N entries.  No gene positive in every sample -> CMC_ERR_CONFIG

@@ -89,6 +89,40 @@ inline CountMatrix load_counts(const std::string& path) {
   return m;
 }
 
+// DesignTable / load_model_matrix (P:src/io.cpp:178-205): X is N x L
+// row-major, effects the header labels; throws LoadError.
+struct DesignTable {
+  long N = 0, L = 0;
+  std::vector<double> X;
+  std::vector<std::string> effects;
+};
+
+inline DesignTable load_model_matrix(const std::string& path) {
+  cmc_table* t = nullptr;
+  cmc_error e{};
+  check(cmc_model_matrix_load(path.c_str(), &t, &e), e);
+  DesignTable d;
+  cmc_table_dims(t, &d.N, &d.L);
+  const double* x = cmc_table_data(t);
+  d.X.assign(x, x + d.N * d.L);
+  for (long l = 0; l < d.L; ++l) d.effects.emplace_back(cmc_table_name(t, l));
+  cmc_table_free(t);
+  return d;
+}
+
+// load_offsets (P:src/io.cpp:221-243); throws LoadError.
+inline std::vector<double> load_offsets(const std::string& path) {
+  cmc_table* t = nullptr;
+  cmc_error e{};
+  check(cmc_offsets_load(path.c_str(), &t, &e), e);
+  long n = 0;
+  cmc_table_dims(t, &n, nullptr);
+  const double* h = cmc_table_data(t);
+  std::vector<double> out(h, h + n);
+  cmc_table_free(t);
+  return out;
+}
+
 // estimate_offsets (P:src/model.cpp:21-68), bit-identical; throws
 // NormalizationError when no gene is positive in every sample.
 inline std::vector<double> estimate_offsets(const CountMatrix& m) {

@@ -144,6 +144,8 @@ def load_ref():
     lib.ref_load_counts.argtypes = [ctypes.c_char_p, POINTER(c_longlong), c_long,
                                     ctypes.c_char_p, c_long, POINTER(c_long), POINTER(c_long),
                                     I, ctypes.c_char_p]
+    lib.ref_load_table.argtypes = [ctypes.c_char_p, c_int, D, c_long, POINTER(c_long),
+                                   POINTER(c_long), ctypes.c_char_p]
     lib.ref_estimate_offsets.argtypes = [c_long, c_long, POINTER(c_longlong), D,
                                          ctypes.c_char_p]
     _REF = lib
@@ -378,6 +380,21 @@ def ref_load_counts(path):
         samples = [p.decode(errors="surrogateescape") for p in parts[:N]]
         genes = [p.decode(errors="surrogateescape") for p in parts[N:]]
         return cells[:G * N].reshape(G, N).copy(), genes, samples, bool(dup.value)
+
+
+def ref_load_table(path, which):
+    """The reference's load_model_matrix (which=0) or load_offsets (1)."""
+    lib = load_ref()
+    cap = 1 << 16
+    out = np.zeros(cap)
+    r, c = c_long(), c_long()
+    msg = ctypes.create_string_buffer(256)
+    rc = lib.ref_load_table(str(path).encode(), which, out.ctypes.data_as(POINTER(c_double)),
+                            cap, ctypes.byref(r), ctypes.byref(c), msg)
+    if rc == 6:
+        raise RefLoadError(msg.value.decode(errors="replace"))
+    assert rc == 0
+    return out[:r.value * c.value].reshape(r.value, c.value).copy()
 
 
 def ref_estimate_offsets(counts):

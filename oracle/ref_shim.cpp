@@ -467,6 +467,31 @@ int ref_load_counts(const char* path, long long* cells, long cap_cells, char* na
   }
 }
 
+// load_model_matrix / load_offsets (P:src/io.cpp:178-243): values into
+// out (capacity cap), dims in rows/cols; 0, 6 (LoadError) or -1 (capacity).
+int ref_load_table(const char* path, int which, double* out, long cap, long* rows, long* cols,
+                   char* msg) {
+  try {
+    std::vector<double> v;
+    if (which == 0) {
+      const DesignTable t = load_model_matrix(path);
+      *rows = static_cast<long>(t.X.rows());
+      *cols = static_cast<long>(t.X.cols());
+      v = t.X.data();
+    } else {
+      v = load_offsets(path);
+      *rows = static_cast<long>(v.size());
+      *cols = 1;
+    }
+    if (cap < static_cast<long>(v.size())) return -1;
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+    return 0;
+  } catch (const LoadError& e) {
+    std::snprintf(msg, 256, "%s", e.what());
+    return 6;
+  }
+}
+
 int ref_estimate_offsets(long G, long N, const long long* counts, double* h, char* msg) {
   CountMatrix m;
   m.counts = Grid<long long>(G, N, 0);

@@ -9,6 +9,7 @@ from .engine import (ChainOutput, ChainState, ConfigError, ContrastSpec, Diagnos
                      ContrastTerm, CountMatrix, DeviceError, GibbsEngine,
                      LoadError, ModelSpec, Moments, NormalizationError, ParamRef,
                      PriorConfig, RunConfig, estimate_offsets, load_counts,
+                     DesignTable, load_model_matrix, load_offsets,
                      SamplerStallError, SimSpec, SliceConfig, TuningState,
                      builtin_design, disjunction_combine, generate,
                      heterosis_contrast, parse_param_ref)
@@ -18,6 +19,7 @@ __all__ = [
     "ChainOutput", "ChainState", "ConfigError", "ContrastSpec", "ContrastTerm", "Diagnostics",
     "CountMatrix", "DeviceError", "GibbsEngine", "LoadError", "ModelSpec", "Moments",
     "NormalizationError", "estimate_offsets", "load_counts",
+    "DesignTable", "load_model_matrix", "load_offsets",
     "ParamRef", "PriorConfig", "RunConfig", "SamplerStallError", "SimSpec",
     "SliceConfig", "TuningState", "builtin_design", "disjunction_combine",
     "generate", "heterosis_contrast", "parse_param_ref", "load_library", "sizes",

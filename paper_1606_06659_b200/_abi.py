@@ -41,6 +41,8 @@ EXPORTS = [
     "cmc_simulate", "cmc_engine_shard", "cmc_nccl_unique_id", "cmc_shard_bounds",
     "cmc_counts_load", "cmc_counts_dims", "cmc_counts_data", "cmc_counts_gene",
     "cmc_counts_sample", "cmc_counts_labels", "cmc_counts_free", "cmc_estimate_offsets",
+    "cmc_model_matrix_load", "cmc_offsets_load", "cmc_table_dims", "cmc_table_data",
+    "cmc_table_name", "cmc_table_free",
 ]
 
 
@@ -245,6 +247,15 @@ def load_library(path: str = LIB_PATH):
                                       POINTER(ctypes.c_size_t)]
     lib.cmc_counts_free.argtypes = [c_void_p]
     lib.cmc_counts_free.restype = None
+    lib.cmc_model_matrix_load.argtypes = [ctypes.c_char_p, POINTER(c_void_p), E]
+    lib.cmc_offsets_load.argtypes = [ctypes.c_char_p, POINTER(c_void_p), E]
+    lib.cmc_table_dims.argtypes = [c_void_p, POINTER(c_long), POINTER(c_long)]
+    lib.cmc_table_data.argtypes = [c_void_p]
+    lib.cmc_table_data.restype = POINTER(c_double)
+    lib.cmc_table_name.argtypes = [c_void_p, c_long]
+    lib.cmc_table_name.restype = ctypes.c_char_p
+    lib.cmc_table_free.argtypes = [c_void_p]
+    lib.cmc_table_free.restype = None
     lib.cmc_estimate_offsets.argtypes = [c_long, c_long, POINTER(c_longlong),
                                          POINTER(c_double), E]
     _LIB = lib

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <fcntl.h>
 #include <sys/mman.h>
@@ -32,6 +33,12 @@ struct cmc_counts {
   std::string gene_blob, sample_blob;  // NUL-terminated labels, back to back
   std::vector<size_t> gene_off, sample_off;
   bool duplicate_genes = false;
+};
+
+struct cmc_table {
+  long rows = 0, cols = 0;
+  std::vector<double> data;        // rows x cols
+  std::vector<std::string> names;  // column names (model matrix: effects)
 };
 
 namespace {
@@ -449,6 +456,152 @@ int cmc_counts_labels(const cmc_counts* c, int which, const char** blob, size_t*
 }
 
 void cmc_counts_free(cmc_counts* c) { delete c; }
+
+// ---- the small tables of the input side: read like the reference
+// (std::getline, one trailing '\r' stripped, blank rows skipped), cells by
+// split_csv, numbers by strtod over the whole cell (parse_real,
+// P:src/io.cpp:103-114, errno not consulted).
+namespace {
+
+bool read_line(std::ifstream& in, std::string& line) {
+  if (!std::getline(in, line)) return false;
+  if (!line.empty() && line.back() == '\r') line.pop_back();
+  return true;
+}
+
+bool parse_real(const std::string& cell, double* v) {
+  char* end = nullptr;
+  *v = std::strtod(cell.c_str(), &end);
+  return !cell.empty() && end == cell.c_str() + cell.size();
+}
+
+std::string malformed(const char* what, const std::string& cell, long row, long col) {
+  std::ostringstream msg;
+  msg << "malformed " << what << " '" << cell << "' (row " << row << ", column " << col << ")";
+  return msg.str();
+}
+
+}  // namespace
+
+extern "C" {
+
+// load_model_matrix, P:src/io.cpp:178-205: header = effect names (L cells),
+// one row per sample with L numbers.
+int cmc_model_matrix_load(const char* path, cmc_table** out, cmc_error* err) {
+  if (!path || !out) {
+    set_err(err, CMC_ERR_ARG, "null argument");
+    return CMC_ERR_ARG;
+  }
+  *out = nullptr;
+  std::ifstream in(path);
+  if (!in) {
+    set_err(err, CMC_ERR_LOAD, std::string("cannot open model matrix file '") + path + "'");
+    return CMC_ERR_LOAD;
+  }
+  std::string line;
+  if (!read_line(in, line)) {
+    set_err(err, CMC_ERR_LOAD, std::string("model matrix file '") + path + "' is empty");
+    return CMC_ERR_LOAD;
+  }
+  auto t = std::make_unique<cmc_table>();
+  split_csv(line.data(), line.data() + line.size(), t->names);
+  const long L = (long)t->names.size();
+  std::vector<std::string> parts;
+  long row = 1;
+  while (read_line(in, line)) {
+    ++row;
+    if (line.empty()) continue;
+    split_csv(line.data(), line.data() + line.size(), parts);
+    if ((long)parts.size() != L) {
+      std::ostringstream msg;
+      msg << "model matrix row " << row << " has " << parts.size() << " cells, expected " << L;
+      set_err(err, CMC_ERR_LOAD, msg.str());
+      return CMC_ERR_LOAD;
+    }
+    for (long l = 0; l < L; ++l) {
+      double v;
+      if (!parse_real(parts[(size_t)l], &v)) {
+        set_err(err, CMC_ERR_LOAD, malformed("model matrix entry", parts[(size_t)l], row, l + 1));
+        return CMC_ERR_LOAD;
+      }
+      t->data.push_back(v);
+    }
+    ++t->rows;
+  }
+  if (t->rows == 0) {
+    set_err(err, CMC_ERR_LOAD, "model matrix has no rows");
+    return CMC_ERR_LOAD;
+  }
+  t->cols = L;
+  *out = t.release();
+  return CMC_OK;
+}
+
+// load_offsets, P:src/io.cpp:221-243: header line, then "sample,offset"
+// rows; the offset is the second cell.
+int cmc_offsets_load(const char* path, cmc_table** out, cmc_error* err) {
+  if (!path || !out) {
+    set_err(err, CMC_ERR_ARG, "null argument");
+    return CMC_ERR_ARG;
+  }
+  *out = nullptr;
+  std::ifstream in(path);
+  if (!in) {
+    set_err(err, CMC_ERR_LOAD, std::string("cannot open offsets file '") + path + "'");
+    return CMC_ERR_LOAD;
+  }
+  std::string line;
+  if (!read_line(in, line)) {
+    set_err(err, CMC_ERR_LOAD, std::string("offsets file '") + path + "' is empty");
+    return CMC_ERR_LOAD;
+  }
+  auto t = std::make_unique<cmc_table>();
+  t->names = {"offset"};
+  std::vector<std::string> parts;
+  long row = 1;
+  while (read_line(in, line)) {
+    ++row;
+    if (line.empty()) continue;
+    split_csv(line.data(), line.data() + line.size(), parts);
+    if (parts.size() != 2) {
+      std::ostringstream msg;
+      msg << "offsets row " << row << " has " << parts.size() << " cells, expected 2";
+      set_err(err, CMC_ERR_LOAD, msg.str());
+      return CMC_ERR_LOAD;
+    }
+    double v;
+    if (!parse_real(parts[1], &v)) {
+      set_err(err, CMC_ERR_LOAD, malformed("offset", parts[1], row, 2));
+      return CMC_ERR_LOAD;
+    }
+    t->data.push_back(v);
+    ++t->rows;
+  }
+  if (t->rows == 0) {
+    set_err(err, CMC_ERR_LOAD, "offsets file has no rows");
+    return CMC_ERR_LOAD;
+  }
+  t->cols = 1;
+  *out = t.release();
+  return CMC_OK;
+}
+
+int cmc_table_dims(const cmc_table* t, long* rows, long* cols) {
+  if (!t) return CMC_ERR_ARG;
+  if (rows) *rows = t->rows;
+  if (cols) *cols = t->cols;
+  return CMC_OK;
+}
+
+const double* cmc_table_data(const cmc_table* t) { return t ? t->data.data() : nullptr; }
+
+const char* cmc_table_name(const cmc_table* t, long col) {
+  return (t && col >= 0 && col < (long)t->names.size()) ? t->names[(size_t)col].c_str() : nullptr;
+}
+
+void cmc_table_free(cmc_table* t) { delete t; }
+
+}  // extern "C"
 
 // estimate_offsets, P:src/model.cpp:21-68: log geometric mean per gene over
 // genes positive in every sample, per-sample median of log ratios

@@ -695,6 +695,42 @@ def load_counts(path: str) -> CountMatrix:
     return CountMatrix(counts, genes, samples, bool(dup.value))
 
 
+@dataclass
+class DesignTable:
+    """Reference DesignTable (P:include/countmc/io.hpp:19-22)."""
+    X: np.ndarray        # N x L
+    effects: List[str]
+
+
+def _load_table(fn, path):
+    lib = load_library()
+    h = c_void_p()
+    err = CmcError()
+    _raise(getattr(lib, fn)(str(path).encode(), byref(h), byref(err)), err)
+    try:
+        r, c = c_long(), c_long()
+        lib.cmc_table_dims(h, byref(r), byref(c))
+        data = np.ctypeslib.as_array(lib.cmc_table_data(h), shape=(r.value * c.value,))
+        data = data.astype(np.float64, copy=True).reshape(r.value, c.value)
+        names = [lib.cmc_table_name(h, k).decode(errors="surrogateescape") for k in range(c.value)]
+    finally:
+        lib.cmc_table_free(h)
+    return data, names
+
+
+def load_model_matrix(path: str) -> DesignTable:
+    """load_model_matrix (P:src/io.cpp:178-205): effect names from the
+    header, one row of L numbers per sample; LoadError like the reference."""
+    X, effects = _load_table("cmc_model_matrix_load", path)
+    return DesignTable(X, effects)
+
+
+def load_offsets(path: str) -> np.ndarray:
+    """load_offsets (P:src/io.cpp:221-243): "sample,offset" rows."""
+    h, _ = _load_table("cmc_offsets_load", path)
+    return h[:, 0].copy()
+
+
 def estimate_offsets(counts) -> np.ndarray:
     """Median-of-ratios log offsets h (reference estimate_offsets,
     P:src/model.cpp:21-68, bit-identical); raises NormalizationError when no

@@ -173,3 +173,61 @@ def test_loaded_file_drives_offsets(tmp_path):
     counts, _, _ = heterosis(3000, seed=9)
     m = load_counts(_write(tmp_path, _csv(counts)))
     assert not len(mismatch(estimate_offsets(m), oracle.ref_estimate_offsets(counts)))
+
+
+# ---- load_model_matrix / load_offsets (P:src/io.cpp:178-243)
+
+def _same_table(path, which, fn):
+    try:
+        ref = oracle.ref_load_table(path, which)
+    except oracle.RefLoadError as e:
+        with pytest.raises(LoadError) as ours:
+            fn(path)
+        assert str(ours.value) == str(e)
+        return None
+    got = fn(path)
+    got = got.X if which == 0 else got[:, None]
+    assert got.shape == ref.shape and not len(mismatch(got.ravel(), ref.ravel()))
+    return got
+
+
+@pytest.mark.parametrize("text", [
+    "a,b,c\n1,0,1\n1,1,-1\n1,-1,0.5\n",
+    "\"x,1\",y\r\n1,2.5e-3\r\n\r\n1,-0x1p3\r\n1, 7\n",   # quoted header, CRLF, hex, blank
+    "a,b\n1,inf\n1,nan\n",                             # strtod accepts these (validation is later)
+    "",
+    "a,b\n",
+    "a,b\n1,2,3\n",
+    "a,b\n1,x\n",
+    "a,b\n1,\n",
+    "a,b\n1,2 \n",
+])
+def test_model_matrix_loader_matches_reference(tmp_path, text):
+    from paper_1606_06659_b200 import load_model_matrix
+    p = _write(tmp_path, text)
+    got = _same_table(p, 0, load_model_matrix)
+    if got is not None and text.startswith('"x,1"'):
+        assert load_model_matrix(p).effects == ["x,1", "y"]
+
+
+@pytest.mark.parametrize("text", [
+    "sample,offset\ns1,0.1\ns2,-0.25\n\ns3,1e-300\n",
+    "sample,offset\r\n\"s,1\",2\r\n",
+    "",
+    "sample,offset\n",
+    "sample,offset\ns1\n",
+    "sample,offset\ns1,0.1,3\n",
+    "sample,offset\ns1,abc\n",
+])
+def test_offsets_loader_matches_reference(tmp_path, text):
+    from paper_1606_06659_b200 import load_offsets
+    p = _write(tmp_path, text)
+    _same_table(p, 1, load_offsets)
+
+
+def test_table_loaders_missing_files(tmp_path):
+    from paper_1606_06659_b200 import load_model_matrix, load_offsets
+    with pytest.raises(LoadError, match="cannot open model matrix file"):
+        load_model_matrix(str(tmp_path / "no.csv"))
+    with pytest.raises(LoadError, match="cannot open offsets file"):
+        load_offsets(str(tmp_path / "no.csv"))
