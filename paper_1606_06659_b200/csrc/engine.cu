@@ -718,6 +718,20 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
   return CMC_OK;
 }
 
+// Debug aid: build with -DCMC_DEBUG_SYNC to synchronise and report after
+// each sweep-kernel launch of enqueue_sweep_on (locates a faulting kernel).
+#ifdef CMC_DEBUG_SYNC
+#define DBG_SYNC(what)                                                             \
+  do {                                                                             \
+    cudaError_t d_ = cudaDeviceSynchronize();                                      \
+    std::fprintf(stderr, "[dbg] %s: %s\n", what, cudaGetErrorString(d_));          \
+  } while (0)
+#else
+#define DBG_SYNC(what) \
+  do {                 \
+  } while (0)
+#endif
+
 // Enqueue one sweep (iteration *d_m + off) for `chains` chains at
 // slot_base.  The gene-phase kernels run on the engine stream; the
 // reduction/hyper tail runs on tail_stream after ev_gene, so the NEXT
@@ -731,17 +745,6 @@ cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p_in, int chains,
   // this launch's chains own a contiguous section of the partial buffers:
   // [world][chains][Q][lpr] at world * slot_base * Q * lpr
   SweepParams p = p_in;
-#ifdef CMC_DEBUG_SYNC
-#define DBG_SYNC(what)                                                             \
-  do {                                                                             \
-    cudaError_t d_ = cudaDeviceSynchronize();                                      \
-    std::fprintf(stderr, "[dbg] %s: %s\n", what, cudaGetErrorString(d_));          \
-  } while (0)
-#else
-#define DBG_SYNC(what) \
-  do {                 \
-  } while (0)
-#endif
   const int Q = leaf_q_a((int)e->L, e->xi_any ? 1 : 0);
   const size_t lpr = (size_t)p.leaves_per_rank, W = (size_t)e->world;
 #ifndef CMC_BISECT_NOOFF
