@@ -281,6 +281,18 @@ int cmc_nccl_unique_id(void* out128, cmc_error* err);
 /* Shard bounds for gene count G over `world` ranks (leaf aligned). */
 int cmc_shard_bounds(long G, int rank, int world, long* g_begin, long* g_end);
 
+/* Test hook, no reference counterpart: an in-process stand-in for the
+ * clique.  `world` engines of one process (one device, one host thread
+ * each) join a loopback group in place of cmc_engine_shard and run the
+ * sharded path as ranks 0..world-1; the all-gather becomes event-ordered
+ * device copies between the engines with a host barrier per exchange.
+ * Eager launches and one chain lane only; for parity tests on one GPU. */
+typedef struct cmc_loopback cmc_loopback;
+int cmc_loopback_create(int world, cmc_loopback** out, cmc_error* err);
+int cmc_loopback_destroy(cmc_loopback* group);
+int cmc_engine_shard_loopback(cmc_engine* engine, int rank, cmc_loopback* group,
+                              cmc_error* err);
+
 /* Results files, replaces countmc::write_results (P:src/io.cpp:571-720):
  * gene_estimates.csv, hyper_estimates.csv, diagnostics.csv,
  * samples/chain_<c>.csv and run_report.json under outdir, from the

@@ -7,7 +7,7 @@ the C-ABI in ``include/countmc_b200.h``; this package mirrors the reference's
 """
 from .engine import (ChainOutput, ChainState, ConfigError, ContrastSpec, Diagnostics,
                      ContrastTerm, CountMatrix, DeviceError, GibbsEngine,
-                     LoadError, ModelSpec, Moments, NormalizationError, ParamRef,
+                     LoadError, LoopbackGroup, ModelSpec, Moments, NormalizationError, ParamRef,
                      PriorConfig, RunConfig, estimate_offsets, load_counts,
                      DesignTable, load_model_matrix, load_offsets,
                      SamplerStallError, SimSpec, SliceConfig, TuningState,
@@ -17,7 +17,8 @@ from ._abi import load_library, sizes
 
 __all__ = [
     "ChainOutput", "ChainState", "ConfigError", "ContrastSpec", "ContrastTerm", "Diagnostics",
-    "CountMatrix", "DeviceError", "GibbsEngine", "LoadError", "ModelSpec", "Moments",
+    "CountMatrix", "DeviceError", "GibbsEngine", "LoadError", "LoopbackGroup", "ModelSpec",
+    "Moments",
     "NormalizationError", "estimate_offsets", "load_counts",
     "DesignTable", "load_model_matrix", "load_offsets",
     "ParamRef", "PriorConfig", "RunConfig", "SamplerStallError", "SimSpec",

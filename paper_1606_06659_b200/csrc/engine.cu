@@ -10,7 +10,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -175,6 +177,36 @@ struct DevBuf {
 #define CMC_MAX_LANES 2
 #endif
 
+// In-process stand-in for the NCCL clique (test hook): W engines of one
+// process share one device, each driven by its own host thread, and play
+// ranks 0..W-1 of a sharded job.  The all-gather becomes stream-ordered
+// device copies between the engines' partial buffers, sequenced by CUDA
+// events and a host barrier -- no kernel waits on another -- so the whole
+// sharded path (leaf-aligned shard bounds, g0-offset RNG sites, the
+// [world][C][Q][lpr] partial sections, the standalone hyper kernels) runs
+// at world > 1 on one GPU.  Eager launches only (events of another
+// engine's stream cannot enter a graph capture), one chain lane.
+struct cmc_loopback {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long gen = 0;
+  std::vector<const double*> send;
+  std::vector<cudaEvent_t> ready, copied;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct cmc_engine {
   // problem (host copy of the full problem)
   long G_total = 0, N = 0, L = 0;
@@ -202,6 +234,8 @@ struct cmc_engine {
   // the lanes' all-gathers never interleave on one communicator
   nccl_comm lane_comm[4] = {nullptr, nullptr, nullptr, nullptr};
   int split_lanes = 1;      // lanes of a sharded engine
+  cmc_loopback* loop = nullptr;  // test hook: in-process exchange instead of NCCL
+  cudaEvent_t loop_ready = nullptr, loop_copied = nullptr;
   bool split_tail = false;  // NCCL exchange between the leaf and hyper kernels
   // device
   int device = 0;
@@ -738,6 +772,40 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
 // sweep's eps kernel (which reads only beta and gamma of this sweep) overlaps
 // it, and the next gene kernel waits for ev_tail (it reads nu, tau, theta,
 // sigma).  In a CUDA graph capture the two streams become parallel branches.
+// The all-gather of one lane's partial sections: part = [world][count],
+// this rank's section at rank * count.  NCCL, or the in-process loopback.
+cudaError_t all_gather_parts(cmc_engine* e, double* part, size_t count, nccl_comm comm,
+                             cudaStream_t t) {
+  if (!e->loop) {
+    if (g_nccl.all_gather(part + (size_t)e->rank * count, part, count, kNcclFloat64, comm, t) != 0)
+      return cudaErrorUnknown;
+    return cudaSuccess;
+  }
+  cmc_loopback& g = *e->loop;
+  const int r = e->rank;
+  cudaError_t rc = cudaEventRecord(e->loop_ready, t);
+  if (rc != cudaSuccess) return rc;
+  g.send[(size_t)r] = part + (size_t)r * count;
+  g.ready[(size_t)r] = e->loop_ready;
+  g.barrier();  // every section published
+  for (int q = 0; q < g.world; ++q) {
+    if (q == r) continue;
+    if ((rc = cudaStreamWaitEvent(t, g.ready[(size_t)q], 0)) != cudaSuccess) return rc;
+    if ((rc = cudaMemcpyAsync(part + (size_t)q * count, g.send[(size_t)q], count * sizeof(double),
+                              cudaMemcpyDeviceToDevice, t)) != cudaSuccess)
+      return rc;
+  }
+  if ((rc = cudaEventRecord(e->loop_copied, t)) != cudaSuccess) return rc;
+  g.copied[(size_t)r] = e->loop_copied;
+  g.barrier();  // every copy enqueued: a peer re-records its events only
+                // after the next exchange's first barrier, i.e. after ours
+  // this rank's section is not overwritten (next sweep's leaf kernel)
+  // before every peer has copied it
+  for (int q = 0; q < g.world; ++q)
+    if (q != r && (rc = cudaStreamWaitEvent(t, g.copied[(size_t)q], 0)) != cudaSuccess) return rc;
+  return cudaSuccess;
+}
+
 cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p_in, int chains,
                              long off, cudaStream_t s, cudaStream_t t,
                              cudaEvent_t ev_gene, cudaEvent_t ev_tail,
@@ -771,14 +839,10 @@ cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p_in, int chains,
     const size_t cA = (size_t)chains * Q * lpr;
     const size_t cB = (size_t)chains * e->L * lpr;
     if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
-    if (g_nccl.all_gather(p.partA + (size_t)e->rank * cA, p.partA, cA, kNcclFloat64, comm, t) !=
-        0)
-      return cudaErrorUnknown;
+    if ((r = all_gather_parts(e, p.partA, cA, comm, t)) != cudaSuccess) return r;
     if ((r = launch_hyper_a(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
-    if (g_nccl.all_gather(p.partB + (size_t)e->rank * cB, p.partB, cB, kNcclFloat64, comm, t) !=
-        0)
-      return cudaErrorUnknown;
+    if ((r = all_gather_parts(e, p.partB, cB, comm, t)) != cudaSuccess) return r;
     if ((r = launch_hyper_b(p, chains, off, t)) != cudaSuccess) return r;
   }
   if (p.monitor_enabled && e->has_ctab && e->ctab.gene_needs_hyper)
@@ -1113,6 +1177,8 @@ int cmc_engine_destroy(cmc_engine* e) {
     if (e->ev1) cudaEventDestroy(e->ev1);
     cudaStreamDestroy(e->stream);
   }
+  if (e->loop_ready) cudaEventDestroy(e->loop_ready);
+  if (e->loop_copied) cudaEventDestroy(e->loop_copied);
   for (int k = 1; k < 4; ++k)
     if (e->lane_comm[k] && g_nccl.destroy) g_nccl.destroy(e->lane_comm[k]);
   if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
@@ -1272,7 +1338,7 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
   const long chunk = CMC_GRAPH_CHUNK;
   CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
   long done = 0;
-  if (total >= chunk) {
+  if (total >= chunk && !e->loop) {
     if (!e->graph || e->graph_len != chunk) {
       if (e->graph) cudaGraphExecDestroy(e->graph);
       e->graph = nullptr;
@@ -1753,6 +1819,10 @@ int cmc_engine_shard(cmc_engine* e, int rank, int world, const void* uid,
     set_err(err, CMC_ERR_CONFIG, "shard has no genes: use fewer ranks for this G");
     return CMC_ERR_CONFIG;
   }
+  if (e->loop) {
+    set_err(err, CMC_ERR_ARG, "engine already joined a loopback group");
+    return CMC_ERR_ARG;
+  }
   e->rank = rank;
   e->world = world;
   e->g0 = b;
@@ -1784,6 +1854,53 @@ int cmc_engine_shard(cmc_engine* e, int rank, int world, const void* uid,
       e->split_lanes = k;
     }
   }
+  return CMC_OK;
+}
+
+int cmc_loopback_create(int world, cmc_loopback** out, cmc_error* err) {
+  if (world < 1 || !out) {
+    set_err(err, CMC_ERR_ARG, "bad world or output pointer");
+    return CMC_ERR_ARG;
+  }
+  cmc_loopback* g = new cmc_loopback;
+  g->world = world;
+  g->send.assign((size_t)world, nullptr);
+  g->ready.assign((size_t)world, nullptr);
+  g->copied.assign((size_t)world, nullptr);
+  *out = g;
+  return CMC_OK;
+}
+
+int cmc_loopback_destroy(cmc_loopback* g) {
+  delete g;
+  return CMC_OK;
+}
+
+int cmc_engine_shard_loopback(cmc_engine* e, int rank, cmc_loopback* g, cmc_error* err) {
+  if (!e || !g || rank < 0 || rank >= g->world) {
+    set_err(err, CMC_ERR_ARG, "bad rank or loopback group");
+    return CMC_ERR_ARG;
+  }
+  if (e->dev_ready || e->comm || e->loop) {
+    set_err(err, CMC_ERR_ARG, "cmc_engine_shard_loopback must precede device use and sharding");
+    return CMC_ERR_ARG;
+  }
+  long b = 0, en = 0;
+  cmc_shard_bounds(e->G_total, rank, g->world, &b, &en);
+  if (en <= b) {
+    set_err(err, CMC_ERR_CONFIG, "shard has no genes: use fewer ranks for this G");
+    return CMC_ERR_CONFIG;
+  }
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaEventCreateWithFlags(&e->loop_ready, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&e->loop_copied, cudaEventDisableTiming));
+  e->rank = rank;
+  e->world = g->world;
+  e->g0 = b;
+  e->G = en - b;
+  e->loop = g;
+  e->split_tail = true;
+  e->split_lanes = 1;
   return CMC_OK;
 }
 

@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(kGeneThreads, CMC_GENE_MIN_BLOCKS)
       const double gam = p.gam[so * G + gl];
       for (int ci = 0; ci < p.ctab_n; ++ci)
         if (t->per_gene[ci])
-          contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + gl,
+          contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + p.g0 + gl,
                           mcount, beta, G, gl, gam, hp);
     }
     // thinning of saved genes, P:src/engine.cpp:433-447
@@ -1194,7 +1194,7 @@ __global__ void gene_contrast_kernel(const SweepParams p, const long m_off) {
   const double gam = p.gam[so * G + gl];
   for (int ci = 0; ci < p.ctab_n; ++ci)
     if (t->per_gene[ci])
-      contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + gl, mc,
+      contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + p.g0 + gl, mc,
                       beta, G, gl, gam, hp);
 }
 

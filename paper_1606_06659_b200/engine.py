@@ -378,6 +378,25 @@ def disjunction_combine(p1, p2, p12):
 
 # -------------------------------------------------------------------- engine
 
+class LoopbackGroup:
+    """Test hook (no reference counterpart): `world` engines of this process
+    on one GPU play the ranks of a sharded job; see cmc_loopback_create."""
+
+    def __init__(self, world: int):
+        self._lib = load_library()
+        self.world = world
+        h = c_void_p()
+        err = CmcError()
+        _raise(self._lib.cmc_loopback_create(world, byref(h), byref(err)), err)
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self._lib.cmc_loopback_destroy(h)
+            self.handle = None
+
+
 class GibbsEngine:
     """B200 GibbsEngine: same constructor, methods and errors as the
     reference (P:include/countmc/engine.hpp:110-159)."""
@@ -442,6 +461,17 @@ class GibbsEngine:
         lo, hi = c_long(), c_long()
         self._lib.cmc_shard_bounds(self.G, rank, world, byref(lo), byref(hi))
         self.shard_range = (lo.value, hi.value)
+
+    def shard_loopback(self, rank: int, group: "LoopbackGroup"):
+        """Test hook: join an in-process loopback group as `rank` instead of
+        an NCCL clique (cmc_engine_shard_loopback).  Each engine of the
+        group must then be driven from its own thread; eager sweeps only."""
+        err = CmcError()
+        _raise(self._lib.cmc_engine_shard_loopback(self._h, rank, group.handle, byref(err)), err)
+        lo, hi = c_long(), c_long()
+        self._lib.cmc_shard_bounds(self.G, rank, group.world, byref(lo), byref(hi))
+        self.shard_range = (lo.value, hi.value)
+        self._loopback = group  # keep the group alive while the engine is
 
     @staticmethod
     def nccl_unique_id() -> bytes:
