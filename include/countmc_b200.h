@@ -268,6 +268,16 @@ int cmc_simulate(long G, long N, long L, const double* X, const double* h,
                  const double* sigma, uint64_t seed, long long* counts_out,
                  cmc_error* err);
 
+/* Loads one chain's ChainOutput (the layout cmc_engine_get_output fills;
+ * every pointer but final_state, contrast_prob, samples and clamp_events is
+ * required) into an unsharded engine of the full problem, as if its own
+ * run() had produced it: how a sharded job's results, gathered and merged
+ * on one rank, reach cmc_engine_diagnostics / cmc_engine_write_results.
+ * Every chain must carry the same monitored count.  No reference
+ * counterpart (the reference has no sharding). */
+int cmc_engine_set_output(cmc_engine* engine, long chain, const cmc_output_view* out,
+                          cmc_error* err);
+
 /* Gene sharding (multi-GPU, one process per GPU): restricts the engine to
  * genes [g_begin, g_end) of the full problem (g_begin a multiple of 1024,
  * the reference reduction leaf, parallel.hpp:60) and joins an NCCL clique

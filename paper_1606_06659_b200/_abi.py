@@ -40,6 +40,7 @@ EXPORTS = [
     "cmc_engine_get_output",
     "cmc_simulate", "cmc_engine_shard", "cmc_nccl_unique_id", "cmc_shard_bounds",
     "cmc_loopback_create", "cmc_loopback_destroy", "cmc_engine_shard_loopback",
+    "cmc_engine_set_output",
     "cmc_counts_load", "cmc_counts_dims", "cmc_counts_data", "cmc_counts_gene",
     "cmc_counts_sample", "cmc_counts_labels", "cmc_counts_free", "cmc_estimate_offsets",
     "cmc_model_matrix_load", "cmc_offsets_load", "cmc_table_dims", "cmc_table_data",
@@ -239,6 +240,7 @@ def load_library(path: str = LIB_PATH):
     lib.cmc_loopback_create.argtypes = [c_int, POINTER(c_void_p), E]
     lib.cmc_loopback_destroy.argtypes = [c_void_p]
     lib.cmc_engine_shard_loopback.argtypes = [c_void_p, c_int, c_void_p, E]
+    lib.cmc_engine_set_output.argtypes = [c_void_p, c_long, POINTER(CmcOutputView), E]
     lib.cmc_counts_load.argtypes = [ctypes.c_char_p, POINTER(c_void_p), E]
     lib.cmc_counts_dims.argtypes = [c_void_p, POINTER(c_long), POINTER(c_long), POINTER(c_int)]
     lib.cmc_counts_data.argtypes = [c_void_p]

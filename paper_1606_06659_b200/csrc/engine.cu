@@ -1540,7 +1540,8 @@ int cmc_engine_diagnostics(cmc_engine* e, const cmc_diag_view* o, cmc_error* err
   if (e->C < 2) return fail_config(err, "gelman_rhat needs at least 2 chains");
   if (e->C > 32) return fail_config(err, "diagnostics support at most 32 chains");
   if (e->split_tail) {
-    set_err(err, CMC_ERR_ARG, "diagnostics of a sharded engine: gather the shards first");
+    set_err(err, CMC_ERR_ARG, "diagnostics of a sharded engine: merge the ranks' outputs into an unsharded engine "
+                "(cmc_engine_set_output; Python: shards.gather_shard_outputs + load_outputs)");
     return CMC_ERR_ARG;
   }
   const long count = monitored_count(e);
@@ -1570,7 +1571,8 @@ int cmc_engine_write_results(cmc_engine* e, const char* outdir, const char* cons
     return CMC_ERR_ARG;
   }
   if (e->split_tail) {
-    set_err(err, CMC_ERR_ARG, "write_results of a sharded engine: gather the shards first");
+    set_err(err, CMC_ERR_ARG, "write_results of a sharded engine: merge the ranks' outputs into an unsharded engine "
+                "(cmc_engine_set_output; Python: shards.gather_shard_outputs + load_outputs)");
     return CMC_ERR_ARG;
   }
   if (e->C > 32) return fail_config(err, "diagnostics support at most 32 chains");
@@ -1785,6 +1787,82 @@ int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,
     for (int k = 0; k < 7; ++k) o->step_seconds[k] = 0.0;
     o->step_seconds[0] = e->sweep_seconds;
   }
+  return CMC_OK;
+}
+
+// The inverse of cmc_engine_get_output, for results of a sharded job: the
+// ranks' outputs, merged on the host, are loaded into an unsharded engine
+// of the full problem, whose device diagnostics and results writer then
+// run as after its own run().
+int cmc_engine_set_output(cmc_engine* e, long chain, const cmc_output_view* o,
+                          cmc_error* err) {
+  if (!e || !o || chain < 0 || chain >= e->C || !o->acc_count || !o->acc_mean ||
+      !o->acc_meansq || !o->acc_mean_c || !o->acc_meansq_c) {
+    set_err(err, CMC_ERR_ARG, "bad chain or incomplete output view");
+    return CMC_ERR_ARG;
+  }
+  if (e->split_tail) {
+    set_err(err, CMC_ERR_ARG, "set_output needs an unsharded engine of the full problem");
+    return CMC_ERR_ARG;
+  }
+  const long count = *o->acc_count;
+  if (count < 0 || count > e->cfg.iterations) {
+    set_err(err, CMC_ERR_ARG, "monitored count out of range");
+    return CMC_ERR_ARG;
+  }
+  if (e->begun && chain > 0 && monitored_count(e) != count) {
+    set_err(err, CMC_ERR_ARG, "every chain needs the same monitored count");
+    return CMC_ERR_ARG;
+  }
+  int rc = ensure_device(e, err);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(e->device));
+  const long G = e->G, N = e->N, L = e->L;
+  const size_t so = (size_t)chain;
+  if (o->final_state && (rc = upload_state(e, chain, o->final_state, nullptr, nullptr, err)))
+    return rc;
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  Hyper hp;
+  CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + chain, sizeof(Hyper), cudaMemcpyDeviceToHost));
+  const double* src[4] = {o->acc_mean, o->acc_meansq, o->acc_mean_c, o->acc_meansq_c};
+  for (int k = 0; k < 4; ++k) {
+    const double* a = src[k];
+    long i = 0;
+    hp.acc[k][0] = a[i++];
+    hp.acc[k][1] = a[i++];
+    for (long l = 0; l < 2 * L; ++l) hp.acc[k][2 + l] = a[i++];
+    CUDA_TRY(aos_to_device(e, a + i, e->acc_beta.p + so * 4 * L * G + (size_t)k * L * G, L));
+    i += G * L;
+    CUDA_TRY(cudaMemcpyAsync(e->acc_gam.p + so * 4 * G + (size_t)k * G, a + i,
+                             sizeof(double) * G, cudaMemcpyHostToDevice, e->stream));
+    i += G;
+    CUDA_TRY(aos_to_device(e, a + i, e->acc_eps.p + so * 4 * N * G + (size_t)k * N * G, N));
+    i += G * N;
+    if (e->xi_any)
+      CUDA_TRY(aos_to_device(e, a + i, e->acc_xi.p + so * 4 * L * G + (size_t)k * L * G, L));
+  }
+  if (o->clamp_events) hp.clamps = *o->clamp_events;
+  hp.err_key = kNoError;
+  hp.err_key_eps = kNoError;
+  CUDA_TRY(cudaMemcpyAsync(e->hyper.p + chain, &hp, sizeof(Hyper), cudaMemcpyHostToDevice,
+                           e->stream));
+  if (e->has_ctab && o->contrast_prob)
+    CUDA_TRY(cudaMemcpyAsync(e->cprob.p + so * e->ctab.n_prob, o->contrast_prob,
+                             sizeof(double) * e->ctab.n_prob, cudaMemcpyHostToDevice, e->stream));
+  if (e->n_cols * e->n_rows > 0) {
+    // host [col][rows] (completed rows only) -> device [col][n_rows]
+    const long rows = std::min<long>(e->n_rows, count / e->cfg.thin);
+    std::vector<double> buf((size_t)e->n_cols * e->n_rows, 0.0);
+    if (o->samples)
+      for (long c = 0; c < e->n_cols; ++c)
+        for (long r = 0; r < rows; ++r) buf[(size_t)c * e->n_rows + r] = o->samples[c * rows + r];
+    CUDA_TRY(cudaMemcpyAsync(e->samples.p + so * e->n_cols * e->n_rows, buf.data(),
+                             sizeof(double) * buf.size(), cudaMemcpyHostToDevice, e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  e->host_m = e->cfg.burnin + count + 1;  // monitored_count() == count
+  e->begun = true;
   return CMC_OK;
 }
 

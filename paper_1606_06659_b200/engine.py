@@ -620,6 +620,37 @@ class GibbsEngine:
         """A TuningState of this engine's layout at w_init."""
         return TuningState(self.G, self.N, self.L, self._cfg.slice.w_init, self.xi)
 
+    def load_outputs(self, outputs: Sequence[ChainOutput]) -> None:
+        """Adopt finished ChainOutputs as this engine's run() result
+        (cmc_engine_set_output): for a sharded job's outputs, merged by
+        shards.merge_shard_outputs, in an unsharded engine of the full
+        problem.  diagnostics() and write_results() then work as after
+        run().  Not in the reference (which has no sharding)."""
+        if len(outputs) != self._cfg.chains:
+            raise ConfigError(f"need {self._cfg.chains} chain outputs, got {len(outputs)}")
+        G, N, L = self.G, self.N, self.L
+        for c, o in enumerate(outputs):
+            moms = [o.nu_acc, o.tau_acc, o.theta_acc, o.sigma_acc, o.beta_acc, o.gamma_acc,
+                    o.eps_acc] + ([o.xi_acc] if self.xi else [])
+            accs = [np.ascontiguousarray(np.concatenate(
+                [np.ravel(getattr(m, k)) for m in moms]), dtype=np.float64)
+                for k in ("mean", "meansq", "mean_c", "meansq_c")]
+            count = np.array([o.beta_acc.count], dtype=np.int64)
+            prob = np.ascontiguousarray(np.concatenate(
+                [np.ravel(r.prob) for r in o.contrasts]) if o.contrasts else np.zeros(1))
+            samples = np.ascontiguousarray(np.ravel(o.samples), dtype=np.float64)
+            if samples.size == 0:
+                samples = np.zeros(1)
+            clamps = np.array([o.clamp_events], dtype=np.uint64)
+            final = np.ascontiguousarray(o.final_state.pack(), dtype=np.float64)
+            view = CmcOutputView(lptr(count), dptr(accs[0]), dptr(accs[1]), dptr(accs[2]),
+                                 dptr(accs[3]), dptr(prob), None, dptr(samples), None,
+                                 clamps.ctypes.data_as(ctypes.POINTER(c_uint64)),
+                                 dptr(final), None)
+            err = CmcError()
+            _raise(self._lib.cmc_engine_set_output(self._h, c, byref(view), byref(err)), err)
+        self._outputs = list(outputs)
+
     def _output(self, chain: int) -> ChainOutput:
         G, N, L = self.G, self.N, self.L
         S, _, A = sizes(G, N, L, self.xi)

@@ -131,3 +131,40 @@ def test_rank_without_genes_is_a_config_error():
     e = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg)
     with pytest.raises(ConfigError):
         e.shard_loopback(2, group)
+
+
+def test_sharded_job_results_files_equal_single_engine(tmp_path):
+    """The multi-GPU user flow: every rank runs its shard, the outputs are
+    merged (shards.merge_shard_outputs, what gather_shard_outputs does on
+    rank 0), loaded into an unsharded engine of the full problem
+    (load_outputs), which writes the reference's result files.  Every file
+    equals the one a single unsharded engine writes; run_report.json
+    differs only in its device-time field."""
+    import json
+    from paper_1606_06659_b200.shards import merge_shard_outputs
+    counts, X, h = heterosis(5000, seed=12)
+    cfg = RunConfig(chains=3, burnin=20, iterations=40, thin=5, seed=4, save_genes=10)
+    cons = [heterosis_contrast()]
+    single = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg, contrasts=cons)
+    single.run()
+    single.write_results(str(tmp_path / "single"), wall_seconds=1.5)
+    engines, outs = _run_ranks(counts, X, h, cfg, 3, contrasts=cons)
+    merged = merge_shard_outputs(outs, [e.shard_range for e in engines])
+    res = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg, contrasts=cons)
+    res.load_outputs(merged)
+    res.write_results(str(tmp_path / "sharded"), wall_seconds=1.5)
+    a, b = tmp_path / "single", tmp_path / "sharded"
+    files = sorted(p.relative_to(a) for p in a.rglob("*") if p.is_file())
+    assert files == sorted(p.relative_to(b) for p in b.rglob("*") if p.is_file())
+    for f in files:
+        if f.name == "run_report.json":
+            def strip(j):  # device seconds differ run to run
+                if isinstance(j, dict):
+                    return {k: strip(v) for k, v in j.items() if k != "step_seconds"}
+                return [strip(v) for v in j] if isinstance(j, list) else j
+            assert strip(json.loads((a / f).read_text())) == strip(json.loads((b / f).read_text()))
+        else:
+            assert (a / f).read_bytes() == (b / f).read_bytes(), f
+    da, db = single.diagnostics(), res.diagnostics()
+    for k in ("rhat", "mean", "sd", "ci_lo", "ci_hi", "ess"):
+        assert np.array_equal(getattr(da, k), getattr(db, k), equal_nan=True), k
