@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -192,18 +193,33 @@ struct cmc_loopback {
   std::condition_variable cv;
   int arrived = 0;
   long gen = 0;
+  bool broken = false;  // a rank failed or timed out: every barrier fails
   std::vector<const double*> send;
   std::vector<cudaEvent_t> ready, copied;
-  void barrier() {
+  // false if the group is broken or a peer does not arrive within 120 s (a
+  // rank that failed elsewhere never reaches its next exchange)
+  bool barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
     const long g = gen;
     if (++arrived == world) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return gen != g; });
+      return true;
     }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) ||
+        gen == g) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
   }
 };
 
@@ -783,26 +799,32 @@ cudaError_t all_gather_parts(cmc_engine* e, double* part, size_t count, nccl_com
   }
   cmc_loopback& g = *e->loop;
   const int r = e->rank;
+  auto fail = [&](cudaError_t rc) {
+    g.abort();
+    return rc;
+  };
   cudaError_t rc = cudaEventRecord(e->loop_ready, t);
-  if (rc != cudaSuccess) return rc;
+  if (rc != cudaSuccess) return fail(rc);
   g.send[(size_t)r] = part + (size_t)r * count;
   g.ready[(size_t)r] = e->loop_ready;
-  g.barrier();  // every section published
+  if (!g.barrier()) return cudaErrorTimeout;  // every section published
   for (int q = 0; q < g.world; ++q) {
     if (q == r) continue;
-    if ((rc = cudaStreamWaitEvent(t, g.ready[(size_t)q], 0)) != cudaSuccess) return rc;
+    if ((rc = cudaStreamWaitEvent(t, g.ready[(size_t)q], 0)) != cudaSuccess) return fail(rc);
     if ((rc = cudaMemcpyAsync(part + (size_t)q * count, g.send[(size_t)q], count * sizeof(double),
                               cudaMemcpyDeviceToDevice, t)) != cudaSuccess)
-      return rc;
+      return fail(rc);
   }
-  if ((rc = cudaEventRecord(e->loop_copied, t)) != cudaSuccess) return rc;
+  if ((rc = cudaEventRecord(e->loop_copied, t)) != cudaSuccess) return fail(rc);
   g.copied[(size_t)r] = e->loop_copied;
-  g.barrier();  // every copy enqueued: a peer re-records its events only
-                // after the next exchange's first barrier, i.e. after ours
+  // every copy enqueued: a peer re-records its events only after the next
+  // exchange's first barrier, i.e. after ours
+  if (!g.barrier()) return cudaErrorTimeout;
   // this rank's section is not overwritten (next sweep's leaf kernel)
   // before every peer has copied it
   for (int q = 0; q < g.world; ++q)
-    if (q != r && (rc = cudaStreamWaitEvent(t, g.copied[(size_t)q], 0)) != cudaSuccess) return rc;
+    if (q != r && (rc = cudaStreamWaitEvent(t, g.copied[(size_t)q], 0)) != cudaSuccess)
+      return fail(rc);
   return cudaSuccess;
 }
 

@@ -39,7 +39,8 @@ def _run_ranks(counts, X, h, cfg, world, contrasts=(), priors=None):
         except Exception as ex:  # surfaced below
             errs.append(ex)
 
-    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    # daemon threads: a hung rank cannot keep the test process alive
+    threads = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
     for t in threads:
         t.start()
     for t in threads:
