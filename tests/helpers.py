@@ -74,6 +74,18 @@ class Product:
         if getattr(self, "h", None):
             self.lib.cmc_engine_destroy(self.h)
 
+    def shard_loopback(self, rank, group):
+        """Join an in-process loopback group (cmc_engine_shard_loopback)."""
+        from ctypes import c_long
+        err = CmcError()
+        rc = self.lib.cmc_engine_shard_loopback(self.h, rank, group.handle, byref(err))
+        if rc:
+            raise RuntimeError(err.msg.decode())
+        lo, hi = c_long(), c_long()
+        self.lib.cmc_shard_bounds(self.G, rank, group.world, byref(lo), byref(hi))
+        self.shard_range = (lo.value, hi.value)
+        self.group = group
+
     def initial_state(self, chain):
         S, _, _ = sizes(self.G, self.N, self.L, self.xi)
         st = np.zeros(S)

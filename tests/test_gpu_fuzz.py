@@ -19,11 +19,11 @@ pytestmark = pytest.mark.gpu
 FAMS = ["normal", "laplace", "t", "horseshoe"]
 
 
-def _case(seed):
+def _case(seed, Gs=(1, 3, 31, 127, 128, 129, 700, 1023, 1024, 1025, 2500)):
     rng = np.random.default_rng(seed)
     N = int(rng.integers(2, 40))
     L = int(rng.integers(1, min(N, 16) + 1))
-    G = int(rng.choice([1, 3, 31, 127, 128, 129, 700, 1023, 1024, 1025, 2500]))
+    G = int(rng.choice(list(Gs)))
     if rng.random() < 0.5:
         X = np.column_stack([np.ones(N), rng.choice([-1.0, 0.0, 1.0], size=(N, L - 1))])
     else:
@@ -43,6 +43,10 @@ def _case(seed):
             break
         except ConfigError:
             continue
+    else:  # a last moderate draw: intercept-only effects, light-tailed gamma
+        counts = generate(SimSpec(G=G, N=N, X=X, h=np.zeros(N), nu=20.0, tau=1.0,
+                                  theta=[1.0] + [0.0] * (L - 1), sigma=[0.1] * L,
+                                  seed=seed)).counts
     priors = None
     if rng.random() < 0.35:
         priors = {"beta_prior": [FAMS[int(k)] for k in rng.integers(0, 4, L)],
@@ -97,3 +101,80 @@ def test_random_configuration_run_matches_oracle(seed):
             assert not badk, (seed, c, k, badk[:5])
         assert not len(mismatch(a["prob"], o["prob"])), (seed, c)
         assert a["clamps"][0] == o["clamps"][0]
+
+
+@pytest.mark.parametrize("seed", list(range(_FROM, _FROM + max(1, _N // 3))))
+def test_random_configuration_sharded_equals_unsharded(seed):
+    """Random cases sharded over world 2-4 through the in-process loopback
+    group (tests/test_gpu_loopback.py): every rank's genes, the
+    hyperparameters, accumulators, contrast probabilities and the clamp
+    totals equal one unsharded run(), bit for bit."""
+    import threading
+    from paper_1606_06659_b200 import LoopbackGroup
+    counts, X, h, cfg, cons, priors = _case(5000 + seed, Gs=(1025, 2049, 2500, 3073, 4100, 6000))
+    G, N = counts.shape
+    L = X.shape[1]
+    leaves = (G + 1023) // 1024
+    # worlds whose ceil(leaves / world) sections leave no rank empty
+    worlds = [w for w in (2, 3, 4) if (w - 1) * -(-leaves // w) < leaves]
+    if not worlds:
+        pytest.skip(f"G={G}: {leaves} leaf, nothing to shard")
+    world = worlds[seed % len(worlds)]
+    try:
+        single = Product(counts, X, h, cfg, contrasts=cons, priors=priors).run()
+    except oracle.StallError:
+        pytest.skip("stalling case (the unsharded fuzz covers stalls)")
+    group = LoopbackGroup(world)
+    engs = []
+    for r in range(world):
+        e = Product(counts, X, h, cfg, contrasts=cons, priors=priors)
+        e.shard_loopback(r, group)
+        engs.append(e)
+    outs, errs = [None] * world, []
+
+    def work(r):
+        try:
+            outs[r] = engs[r].run()
+        except Exception as ex:
+            errs.append(ex)
+
+    ts = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in ts) and not errs, errs
+    per_gene = [any(f in ("beta_col", "gamma") for t in c for f, _, _ in t[0]) for c in cons]
+    th0 = G * N + G + G * L
+    h0 = 2 + 2 * L
+    xi = engs[0].xi
+    for c in range(cfg.chains):
+        a = single[c]
+        for r, e in enumerate(engs):
+            lo, hi = e.shard_range
+            b = outs[r][c]
+
+            def same(x, y, what):
+                assert not len(mismatch(x, y)), (seed, world, r, c, what)
+
+            # final state: eps [G][N], gamma [G], beta [G][L], then theta,
+            # sigma, nu, tau, then xi [G][L]
+            for off, k, what in ((0, N, "eps"), (G * N, 1, "gamma"), (G * N + G, L, "beta")) + \
+                    (((th0 + 2 * L + 2, L, "xi"),) if xi else ()):
+                same(a["final"][off + lo * k:off + hi * k], b["final"][off + lo * k:off + hi * k],
+                     what)
+            same(a["final"][th0:th0 + 2 * L + 2], b["final"][th0:th0 + 2 * L + 2], "hyper")
+            # accumulators: hyper, beta [G][L], gamma [G], eps [G][N], xi
+            for k in ("mean", "meansq"):
+                same(a[k][:h0], b[k][:h0], k + " hyper")
+                for off, w, what in ((h0, L, "beta"), (h0 + G * L, 1, "gamma"),
+                                     (h0 + G * L + G, N, "eps")):
+                    same(a[k][off + lo * w:off + hi * w], b[k][off + lo * w:off + hi * w],
+                         f"{k} {what}")
+            off = 0
+            for pg in per_gene:
+                n = G if pg else 1
+                sl = slice(off + lo, off + hi) if pg else slice(off, off + 1)
+                same(a["prob"][sl], b["prob"][sl], "contrast")
+                off += n
+        assert sum(int(outs[r][c]["clamps"][0]) for r in range(world)) == int(a["clamps"][0])
