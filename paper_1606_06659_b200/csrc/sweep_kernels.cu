@@ -27,6 +27,7 @@
 #include "fastmath.cuh"
 #include "rng.cuh"
 #include <cassert>
+#include <type_traits>
 
 #include "sweep.h"
 
@@ -128,7 +129,8 @@ __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
 // bits only, which decides comparisons like libm differences do.  Clamp
 // events are counted only for evaluations the reference performs.  The
 // shrinkage phase uses the full density.  F provides operator() (full),
-// side_init(lo, hi, w), eval_l/eval_r(x, counted) and step_l/step_r().
+// side_init(lo, hi, w), any_fresh(), eval_l/eval_r<FRESH>(x, counted) and
+// step_l/step_r().
 template <class F>
 __device__ __forceinline__ double slice_step_so2(F& f, double x0, double& w,
                                                  double& wa, const SliceCfg& sc,
@@ -143,24 +145,33 @@ __device__ __forceinline__ double slice_step_so2(F& f, double x0, double& w,
   int kl = kl0, kr = sc.K - kl0;
   bool goL = kl > 0, goR = kr > 0;
   f.side_init(lo, hi, wv);
-  while (goL || goR) {
-    const double fl = f.eval_l(lo, goL);
-    const double fr = f.eval_r(hi, goR);
-    const bool inL = goL && logu < fl;
-    const bool inR = goR && logu < fr;
-    if (inL) {
-      lo -= wv;
-      f.step_l();
+  // FRESH: the loop body that can take a fresh exp per side (F::side_init
+  // decides); the common case runs a body without any exp.
+  auto step_out = [&](auto fresh_tag) {
+    constexpr bool FRESH = decltype(fresh_tag)::value;
+    while (goL || goR) {
+      const double fl = f.template eval_l<FRESH>(lo, goL);
+      const double fr = f.template eval_r<FRESH>(hi, goR);
+      const bool inL = goL && logu < fl;
+      const bool inR = goR && logu < fr;
+      if (inL) {
+        lo -= wv;
+        f.step_l();
+      }
+      if (inR) {
+        hi += wv;
+        f.step_r();
+      }
+      kl -= inL ? 1 : 0;
+      kr -= inR ? 1 : 0;
+      goL = inL && kl > 0;
+      goR = inR && kr > 0;
     }
-    if (inR) {
-      hi += wv;
-      f.step_r();
-    }
-    kl -= inL ? 1 : 0;
-    kr -= inR ? 1 : 0;
-    goL = inL && kl > 0;
-    goR = inR && kr > 0;
-  }
+  };
+  if (f.any_fresh())
+    step_out(std::true_type{});
+  else
+    step_out(std::false_type{});
   for (int it = 0;;) {
     const double xs = lo + (hi - lo) * rng.u01();
     if (f(xs) > logu) {
@@ -185,6 +196,7 @@ struct EpsF {
   ExpTab tab;
   unsigned clamps;
   double EL, ER, rL, rR;  // step-out: exp(cn + lo), exp(cn + hi), exp(-w), exp(w)
+  bool fL, fR;            // side evaluates fresh exps (see side_init)
   __device__ __forceinline__ double operator()(double x) {
     const double t = cn + x;
     double e;
@@ -200,20 +212,40 @@ struct EpsF {
     const double tl = cn + lo, th = cn + hi;
     EL = tl > kExpClamp ? 0.0 : fast_exp_le700(tl, tab);
     ER = th > kExpClamp ? 0.0 : fast_exp_le700(th, tab);
-    rR = fast_exp_le700(w, tab);
+    rR = fast_exp_le700(fmin(w, kExpClamp), tab);
     rL = 1.0 / rR;
+    // A side carries E multiplicatively only from a normal start (E above
+    // 1e-290) and with steps within fast_exp_le700's range (w <= 700).
+    // Otherwise -- a side that starts clamped (E = 0 here) or underflowed,
+    // or w > 700 -- it evaluates a fresh exp on every unclamped trip, as
+    // the reference does.  From a normal start the carried E stays valid:
+    // on the right t grows and E is read only while t <= 700 (E <= e^700 <
+    // DBL_MAX); on the left E only shrinks, and once below the normal range
+    // it is far below the last bit of y x - x^2 / (2 gamma).
+    const bool wide = !(w <= kExpClamp);
+    fL = wide || !(EL > 1e-290);
+    fR = wide || !(ER > 1e-290);
   }
-  // value at x with the carried exp E (recomputed if it left the normal
-  // range, e.g. after a clamp or an underflow)
-  __device__ __forceinline__ double side_eval(double x, double& E, bool counted) {
+  // Step-out evaluation at x with the carried exp E (or a fresh one, see
+  // side_init).  The mode is decided once per side: a per-trip range test
+  // on E measured 0.5-2.5% of the sweep.
+  template <bool FRESH>
+  __device__ __forceinline__ double side_eval(double x, double& E, bool fresh, bool counted) {
     const double t = cn + x;
     const bool cl = t > kExpClamp;
-    if (!cl && !(E > 1e-290 && E < 1e290)) E = fast_exp_le700(t, tab);
+    if (FRESH && fresh && !cl) E = fast_exp_le700(t, tab);
     clamps += (cl && counted) ? 1u : 0u;
     return y * x - (cl ? e700 : E) - x * x * inv_two_gam;
   }
-  __device__ __forceinline__ double eval_l(double x, bool c) { return side_eval(x, EL, c); }
-  __device__ __forceinline__ double eval_r(double x, bool c) { return side_eval(x, ER, c); }
+  template <bool FRESH>
+  __device__ __forceinline__ double eval_l(double x, bool c) {
+    return side_eval<FRESH>(x, EL, fL, c);
+  }
+  template <bool FRESH>
+  __device__ __forceinline__ double eval_r(double x, bool c) {
+    return side_eval<FRESH>(x, ER, fR, c);
+  }
+  __device__ __forceinline__ bool any_fresh() const { return fL || fR; }
   __device__ __forceinline__ void step_l() { EL *= rL; }
   __device__ __forceinline__ void step_r() { ER *= rR; }
 };
