@@ -513,6 +513,9 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   Hyper* hp = p.hyper + slot;
   if (stalled_chain(hp)) return;
   const long gl = (long)blockIdx.x * kGeneBlock + threadIdx.x;
+  // lanes with a gene: the warp is re-converged over them after the slice
+  // step (below)
+  const unsigned live = __ballot_sync(0xffffffffu, gl < p.G);
   if (gl >= p.G) return;
   const int n = blockIdx.y;
   const long m = *p.d_m + m_off;
@@ -551,6 +554,11 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
   bool st = false;
   const double x1 = slice_step_so2(f, x0, w, wa, sc, m, rng, st);
+  // The shrink loop's lanes leave at different trips (a return inside the
+  // inlined loop); without an explicit re-convergence point the stores and
+  // the Welford update below ran once per exit group, at ~16 of 32 lanes
+  // (ncu).  Re-converged: 2.4% per sweep.
+  __syncwarp(live);
   if (st) {
     // eps and its width stay untouched: the host reads x0 and w back.
     // The eps kernel of iteration m+1 runs concurrently with the tail of
@@ -817,6 +825,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_MIN_BLOCKS)
   Hyper* hp = p.hyper + slot;
   if (stalled_chain(hp)) return;
   const long gl = (long)blockIdx.x * kGeneBlock + threadIdx.x;
+  const unsigned live = __ballot_sync(0xffffffffu, gl < p.G);
   if (gl >= p.G) return;
   const long m = *p.d_m + m_off;
   const bool tuning = m <= p.burnin;
@@ -835,6 +844,7 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_MIN_BLOCKS)
   rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteXi, gg * L + l));
   bool st = false;
   const double x1 = slice_step(f, p.xi[ix], w, wa, sc, m, rng, st);
+  __syncwarp(live);  // re-converge after the slice loop (as in the eps kernel)
   if (st) {
     record_stall(hp, stall_key(5, l, gg, 1), m);
     return;
