@@ -496,12 +496,15 @@ __device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
 // independent given the gene's previous beta and gamma (P:src/engine.cpp:
 // 178-202), so the 16 slice steps of a gene run on 16 threads.  A warp holds
 // 32 consecutive genes at one sample n (coalesced SoA loads), the grid's y
-// dimension is n and z the chain.  Capped at 64 registers (8 blocks, 32
-// warps per SM; one 8-byte spill): the step is latency-bound, and the extra
-// warps beat the spill (A/B on B200: 6 blocks 4.18e8, 8 blocks 4.31e8
+// dimension is n and z the chain.  The step is latency-bound, so the block
+// count per SM is tuned against spills (earlier A/B on B200: 6 blocks 4.18e8, 8 blocks 4.31e8
 // gene-iter/s, 9-10 blocks no better once the gene kernel also runs at 6).
+// Since the one-decision step-out and the post-step re-convergence, 7
+// blocks (72 registers, no spill) edge out 8 (64 registers, 16-byte
+// spill): 0.3330 vs 0.3338 ms per 4-chain sweep, 0.133 vs 0.136 ms at 1
+// chain (A/B, two reps each).
 #ifndef CMC_EPS_MIN_BLOCKS
-#define CMC_EPS_MIN_BLOCKS 8
+#define CMC_EPS_MIN_BLOCKS 7
 #endif
 __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
     eps_sweep_kernel(const SweepParams p, const long m_off) {
