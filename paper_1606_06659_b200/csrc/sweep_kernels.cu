@@ -211,9 +211,16 @@ struct EpsF {
   __device__ __forceinline__ void side_init(double lo, double hi, double w) {
     const double tl = cn + lo, th = cn + hi;
     EL = tl > kExpClamp ? 0.0 : fast_exp_le700(tl, tab);
-    ER = th > kExpClamp ? 0.0 : fast_exp_le700(th, tab);
     rR = fast_exp_le700(fmin(w, kExpClamp), tab);
     rL = 1.0 / rR;
+    // hi = lo + w: from a normal EL (and w <= 700) ER is one carried step,
+    // the same product the step-out loop forms (no third exp per step)
+    if (th > kExpClamp)
+      ER = 0.0;
+    else if (EL > 1e-290 && w <= kExpClamp)
+      ER = EL * rR;
+    else
+      ER = fast_exp_le700(th, tab);
     // A side carries E multiplicatively only from a normal start (E above
     // 1e-290) and with steps within fast_exp_le700's range (w <= 700).
     // Otherwise -- a side that starts clamped (E = 0 here) or underflowed,
