@@ -73,19 +73,24 @@ def test_widest_model_matrix():
     _pair_sweeps(counts, X, np.zeros(N), cfg, 5)
 
 
-def test_exp_clamp_path_counts_agree():
+@pytest.mark.parametrize("w_init", [1000.0, 690.0])
+def test_exp_clamp_path_counts_agree(w_init):
     """A first slice interval of width 1000 (w_init) puts step-out bounds and
     shrink proposals past h + xb + eps = 700, where clamped_exp returns
     exp(700) and bumps the ClampCounter (P:src/model.cpp:13-19); the device's
     counts equal the oracle's sweep by sweep.  (Offsets near 700 instead make
-    every density ~1e303, which absorbs log(u) and stalls the reference too.)"""
+    every density ~1e303, which absorbs log(u) and stalls the reference too.)
+    Width 690 is within the carried step-out's range but puts the left end
+    of some intervals (placement draw u > ~0.97) below exp's normal range, so the ε step-out takes its
+    fresh-exp path on one side and a carried exp on the other."""
     from paper_1606_06659_b200 import builtin_design
     X = builtin_design("heterosis16x5", 16)
     counts = _sim(500, X, np.zeros(16), 7)
     cfg = _abi.make_config(chains=1, burnin=20, iterations=20, thin=10, seed=8, save_genes=3,
-                           w_init=1000.0)
+                           w_init=w_init)
     clamps = _pair_sweeps(counts, X, np.zeros(16), cfg, 4)
-    assert clamps > 0
+    if w_init > 700.0:
+        assert clamps > 0
 
 
 @pytest.mark.parametrize("G", [1, 127, 129, 1023, 1025, 2049])
