@@ -225,6 +225,14 @@ int cmc_engine_launches_per_sweep(const cmc_engine* engine);
  * the reduction/hyper tail per sweep. */
 int cmc_engine_profile(cmc_engine* engine, long m_begin, long reps,
                        double* gene_ms, double* tail_ms, cmc_error* err);
+/* The same per sweep phase (single GPU): ms[CMC_PHASES] = average device ms
+ * of eps (step 1), gene (steps 2 + 5), xi (extension), leaf_a (reductions
+ * + nu, tau, theta: steps 3, 4, 6), leaf_b (reductions + sigma, step 7, and
+ * the hyper monitors), gene_contrast; each phase one launch for all chains,
+ * phases serialised with CUDA events between them. */
+#define CMC_PHASES 6
+int cmc_engine_profile_phases(cmc_engine* engine, long m_begin, long reps,
+                              double* ms, cmc_error* err);
 
 /* Post-run diagnostics (reference build_diagnostics, src/io.cpp:507-569,
  * over src/diagnostics.cpp), computed on the device from the resident

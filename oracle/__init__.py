@@ -125,6 +125,8 @@ def load_ref():
                                       c_double, D, E]
     lib.ref_bench_split.argtypes = [c_void_p, c_int, c_int, c_long, c_long]
     lib.ref_bench_split.restype = c_double
+    lib.ref_bench_chains.argtypes = [c_void_p, c_int, c_int, c_long, c_long, c_long]
+    lib.ref_bench_chains.restype = c_double
     lib.ref_hardware_threads.restype = c_int
     I = POINTER(c_int)
     lib.ref_diagnostics.argtypes = [c_void_p, D, I, D, D, D, D, D, I, E]
@@ -148,6 +150,9 @@ def load_ref():
                                    POINTER(c_long), ctypes.c_char_p]
     lib.ref_estimate_offsets.argtypes = [c_long, c_long, POINTER(c_longlong), D,
                                          ctypes.c_char_p]
+    lib.ref_generate.argtypes = [c_long, c_long, c_long, D, D, c_double, c_double, D, D,
+                                 c_uint64, POINTER(c_longlong), ctypes.c_char_p]
+    lib.ref_builtin_design.argtypes = [c_long, D]
     _REF = lib
     return lib
 
@@ -338,8 +343,11 @@ class RefEngine(_Base):
             raise StallError(err.msg.decode())
         return secs.value
 
-    def bench(self, workers, burn, sweeps, burn_workers=None):
-        return self.lib.ref_bench_split(self.h, burn_workers or workers, workers, burn, sweeps)
+    def bench(self, workers, burn, sweeps, burn_workers=None, chains=1):
+        """Seconds of `chains` x `sweeps` monitored sweeps (chains in sequence,
+        as run()), each chain after `burn` untimed burn-in sweeps."""
+        return self.lib.ref_bench_chains(self.h, burn_workers or workers, workers, chains,
+                                         burn, sweeps)
 
 
 def heterosis16x5(N=16):
@@ -350,6 +358,34 @@ def heterosis16x5(N=16):
         X[n, :4] = A[(n % 16) // 4]
         X[n, 4] = block[n % 4]
     return X
+
+
+def ref_generate(G, N, nu, tau, theta, sigma, seed, X=None, h=None):
+    """The reference's own synthetic data: generate() (P:src/simulate.cpp:
+    28-90), with builtin_design("heterosis16x5", N) when X is None.
+    Returns (counts G x N int64, X N x L)."""
+    lib = load_ref()
+    if X is None:
+        L = len(theta)
+        X = np.zeros((N, L))
+        lib.ref_builtin_design(N, X.ctypes.data_as(POINTER(c_double)))
+        Xp = None
+    else:
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        L = X.shape[1]
+        Xp = X.ctypes.data_as(POINTER(c_double))
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    sg = np.ascontiguousarray(sigma, dtype=np.float64)
+    hh = None if h is None else np.ascontiguousarray(h, dtype=np.float64)
+    out = np.zeros((G, N), np.int64)
+    msg = ctypes.create_string_buffer(256)
+    rc = lib.ref_generate(G, N, L, Xp, None if hh is None else hh.ctypes.data_as(POINTER(c_double)),
+                          nu, tau, th.ctypes.data_as(POINTER(c_double)),
+                          sg.ctypes.data_as(POINTER(c_double)), seed,
+                          out.ctypes.data_as(POINTER(c_longlong)), msg)
+    if rc:
+        raise ConfigErr(msg.value.decode(errors="replace"))
+    return out, X
 
 
 def ref_load_counts(path):

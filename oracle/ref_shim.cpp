@@ -21,6 +21,7 @@
 #include "countmc/model.hpp"
 #include "countmc/parallel.hpp"
 #include "countmc/rng.hpp"
+#include "countmc/simulate.hpp"
 #include "countmc/slice.hpp"
 #include "countmc/streaming.hpp"
 #include "countmc/types.hpp"
@@ -331,56 +332,69 @@ int ref_write_results(void* h, const char* outdir, const char* const* genes,
 // loop body (P:src/engine.cpp:409-431: moment and contrast accumulators),
 // `burn` un-timed burn-in sweeps then `sweeps` timed sweeps on `workers`
 // threads.  Returns wall seconds of the timed sweeps.
-double ref_bench_split(void* h, int burn_workers, int workers, long burn, long sweeps);
+double ref_bench_chains(void* h, int burn_workers, int workers, long chains, long burn,
+                        long sweeps);
 
 double ref_bench(void* h, int workers, long burn, long sweeps) {
-  return ref_bench_split(h, workers, workers, burn, sweeps);
+  return ref_bench_chains(h, workers, workers, 1, burn, sweeps);
 }
 
 // Burn-in on burn_workers threads, then `sweeps` monitored sweeps timed on
 // `workers` threads (iterate is bitwise independent of the worker count).
-double ref_bench_split(void* h, int burn_workers, int workers, long burn, long sweeps) {
+// `chains` chains run one after another, as run() runs them (chains in
+// sequence on one pool, P:src/engine.cpp:457-483); the timed seconds of
+// every chain's monitored sweeps are summed.
+double ref_bench_chains(void* h, int burn_workers, int workers, long chains, long burn,
+                        long sweeps) {
   auto* r = static_cast<RefEngine*>(h);
   const auto& cfg = r->engine->config();
   const long G = r->G, N = r->N, L = r->L;
-  ChainState state = r->engine->initial_state(0);
-  TuningState tuning(G, N, L, cfg.slice.w_init);
-  EngineScratch scratch(G, N);
-  ClampCounter clamps;
-  std::vector<MomentAccumulator> theta_acc(L), sigma_acc(L), beta_acc(G * L),
-      gamma_acc(G), eps_acc(G * N);
-  MomentAccumulator nu_acc, tau_acc;
-  std::vector<ContrastAccumulator> contrasts;
-  for (const auto& spec : r->engine->contrast_specs()) contrasts.emplace_back(spec, G);
-  {
-    ThreadPool burn_pool(burn_workers);
-    for (long m = 1; m <= burn; ++m)
-      r->engine->iterate(state, tuning, 0, m, burn_pool, scratch, &clamps);
-  }
-  ThreadPool pool(workers);
-  const auto t0 = std::chrono::steady_clock::now();
-  for (long m = burn + 1; m <= burn + sweeps; ++m) {
-    r->engine->iterate(state, tuning, 0, m, pool, scratch, &clamps);
-    nu_acc.update(state.nu);
-    tau_acc.update(state.tau);
-    for (long l = 0; l < L; ++l) {
-      theta_acc[l].update(state.theta[l]);
-      sigma_acc[l].update(state.sigma[l]);
+  double total = 0.0;
+  for (long c = 0; c < chains; ++c) {
+    ChainState state = r->engine->initial_state(c);
+    TuningState tuning(G, N, L, cfg.slice.w_init);
+    EngineScratch scratch(G, N);
+    ClampCounter clamps;
+    std::vector<MomentAccumulator> theta_acc(L), sigma_acc(L), beta_acc(G * L),
+        gamma_acc(G), eps_acc(G * N);
+    MomentAccumulator nu_acc, tau_acc;
+    std::vector<ContrastAccumulator> contrasts;
+    for (const auto& spec : r->engine->contrast_specs()) contrasts.emplace_back(spec, G);
+    {
+      ThreadPool burn_pool(burn_workers);
+      for (long m = 1; m <= burn; ++m)
+        r->engine->iterate(state, tuning, c, m, burn_pool, scratch, &clamps);
     }
-    pool.parallel_for(G, std::max<long>(1, G / (8 * pool.workers())),
-                      [&](long g0, long g1) {
-                        for (long g = g0; g < g1; ++g) {
-                          for (long l = 0; l < L; ++l)
-                            beta_acc[g * L + l].update(state.beta(g, l));
-                          gamma_acc[g].update(state.gamma[g]);
-                          const double* eps = state.eps.row(g);
-                          for (long n = 0; n < N; ++n) eps_acc[g * N + n].update(eps[n]);
-                        }
-                      });
-    for (auto& acc : contrasts) acc.update(state);
+    ThreadPool pool(workers);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long m = burn + 1; m <= burn + sweeps; ++m) {
+      r->engine->iterate(state, tuning, c, m, pool, scratch, &clamps);
+      nu_acc.update(state.nu);
+      tau_acc.update(state.tau);
+      for (long l = 0; l < L; ++l) {
+        theta_acc[l].update(state.theta[l]);
+        sigma_acc[l].update(state.sigma[l]);
+      }
+      pool.parallel_for(G, std::max<long>(1, G / (8 * pool.workers())),
+                        [&](long g0, long g1) {
+                          for (long g = g0; g < g1; ++g) {
+                            for (long l = 0; l < L; ++l)
+                              beta_acc[g * L + l].update(state.beta(g, l));
+                            gamma_acc[g].update(state.gamma[g]);
+                            const double* eps = state.eps.row(g);
+                            for (long n = 0; n < N; ++n) eps_acc[g * N + n].update(eps[n]);
+                          }
+                        });
+      for (auto& acc : contrasts) acc.update(state);
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    total += std::chrono::duration<double>(t1 - t0).count();
   }
-  const auto t1 = std::chrono::steady_clock::now();
-  return std::chrono::duration<double>(t1 - t0).count();
+  return total;
+}
+
+double ref_bench_split(void* h, int burn_workers, int workers, long burn, long sweeps) {
+  return ref_bench_chains(h, burn_workers, workers, 1, burn, sweeps);
 }
 
 // build_diagnostics (P:src/io.cpp:507-569) numerics with the reference's
@@ -538,5 +552,42 @@ double ref_log_fc_sigma(double s, long G, double ss, double sb) {
   return log_fc_sigma(s, G, ss, sb);
 }
 double ref_pairwise_sum(const double* x, long n) { return pairwise_sum(x, n); }
+
+
+// ---- the reference's own synthetic inputs (bench.py's reference arm) ----
+// generate() (P:src/simulate.cpp:28-90) with builtin_design (:123-142) when
+// X is null; counts out as G x N row-major.  0 ok, 1 ConfigError or
+// SimulationError (message in msg).
+int ref_generate(long G, long N, long L, const double* X, const double* h, double nu,
+                 double tau, const double* theta, const double* sigma, uint64_t seed,
+                 long long* counts, char* msg) {
+  try {
+    SimSpec spec;
+    spec.G = (std::size_t)G;
+    spec.N = (std::size_t)N;
+    if (X) {
+      spec.X = Matrix((std::size_t)N, (std::size_t)L, 0.0);
+      std::memcpy(spec.X.data().data(), X, sizeof(double) * N * L);
+    } else {
+      spec.X = builtin_design("heterosis16x5", (std::size_t)N);
+    }
+    if (h) spec.h.assign(h, h + N);
+    spec.nu = nu;
+    spec.tau = tau;
+    spec.theta.assign(theta, theta + spec.L());
+    spec.sigma.assign(sigma, sigma + spec.L());
+    spec.seed = seed;
+    auto out = generate(spec);
+    std::memcpy(counts, out.first.counts.data().data(), sizeof(long long) * G * N);
+    return 0;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, 256, "%s", e.what());
+    return 1;
+  }
+}
+void ref_builtin_design(long N, double* X) {
+  const Matrix m = builtin_design("heterosis16x5", (std::size_t)N);
+  std::memcpy(X, m.data().data(), sizeof(double) * m.size());
+}
 
 }  // extern "C"

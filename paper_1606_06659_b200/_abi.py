@@ -24,6 +24,9 @@ CMC_ERR_NCCL = 4
 CMC_ERR_ARG = 5
 CMC_ERR_LOAD = 6
 
+CMC_PHASES = 6  # eps, gene, xi, leaf_a, leaf_b, gene_contrast
+PHASE_NAMES = ("eps", "gene", "xi", "leaf_a", "leaf_b", "gene_contrast")
+
 CMC_SLICE_FAITHFUL = 0
 CMC_CONJUGATE_DIRECT = 1
 
@@ -36,6 +39,7 @@ EXPORTS = [
     "cmc_engine_set_state", "cmc_engine_get_state", "cmc_engine_iterate",
     "cmc_engine_run", "cmc_engine_begin", "cmc_engine_sweeps", "cmc_engine_sync",
     "cmc_engine_stream", "cmc_engine_launches_per_sweep", "cmc_engine_profile",
+    "cmc_engine_profile_phases",
     "cmc_engine_trace", "cmc_engine_diagnostics", "cmc_engine_write_results",
     "cmc_engine_get_output",
     "cmc_simulate", "cmc_engine_shard", "cmc_nccl_unique_id", "cmc_shard_bounds",
@@ -223,6 +227,7 @@ def load_library(path: str = LIB_PATH):
     lib.cmc_engine_launches_per_sweep.argtypes = [c_void_p]
     lib.cmc_engine_profile.argtypes = [c_void_p, c_long, c_long, POINTER(c_double),
                                        POINTER(c_double), E]
+    lib.cmc_engine_profile_phases.argtypes = [c_void_p, c_long, c_long, POINTER(c_double), E]
     lib.cmc_engine_trace.argtypes = [c_void_p, c_long, c_long, POINTER(ctypes.c_uint64), c_long,
                                      POINTER(c_long), E]
     lib.cmc_engine_diagnostics.argtypes = [c_void_p, POINTER(CmcDiagView), E]

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <random>
 #include <string>
 #include <thread>
 #include <vector>
@@ -284,9 +285,13 @@ struct cmc_engine {
   DevBuf<long> d_m;
   long host_m = 1;  // value of *d_m
   SweepParams base{};
-  // graph cache: chunk length -> exec
-  cudaGraphExec_t graph = nullptr;
-  long graph_len = 0;
+  // graph cache: sweeps per graph -> exec (the 50-sweep chunk of a run,
+  // plus the lengths of shorter sweep calls and of a run's remainder)
+  static constexpr int kGraphSlots = 6;
+  cudaGraphExec_t graph[kGraphSlots] = {};
+  long graph_len[kGraphSlots] = {};
+  long graph_use[kGraphSlots] = {};
+  long graph_clock = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timing_pending = false;
   double sweep_seconds = 0.0;
@@ -924,6 +929,51 @@ cudaError_t join_lanes(cmc_engine* e) {
   return cudaSuccess;
 }
 
+// The executable graph of `len` consecutive sweeps of every lane (iteration
+// *d_m + 0 .. len-1) followed by the advance of *d_m, from the cache or
+// captured now (least recently used slot replaced).
+cudaError_t sweep_graph(cmc_engine* e, const SweepParams& p, long len, cudaGraphExec_t* out) {
+  const int S = cmc_engine::kGraphSlots;
+  ++e->graph_clock;
+  for (int k = 0; k < S; ++k)
+    if (e->graph[k] && e->graph_len[k] == len) {
+      e->graph_use[k] = e->graph_clock;
+      *out = e->graph[k];
+      return cudaSuccess;
+    }
+  int victim = -1;
+  for (int k = 0; k < S && victim < 0; ++k)
+    if (!e->graph[k]) victim = k;
+  if (victim < 0) {
+    victim = 0;
+    for (int k = 1; k < S; ++k)
+      if (e->graph_use[k] < e->graph_use[victim]) victim = k;
+  }
+  if (e->graph[victim]) {
+    cudaError_t r = cudaGraphExecDestroy(e->graph[victim]);
+    e->graph[victim] = nullptr;
+    if (r != cudaSuccess) return r;
+  }
+  cudaGraph_t g;
+  cudaError_t r = cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal);
+  if (r != cudaSuccess) return r;
+  // fork the other lanes and the tail streams into the capture
+  r = fork_lanes(e);
+  for (long off = 0; r == cudaSuccess && off < len; ++off) r = enqueue_all_lanes(e, p, off);
+  if (r == cudaSuccess) r = join_lanes(e);
+  if (r == cudaSuccess) r = launch_advance(e->d_m.p, len, e->stream);
+  cudaError_t r2 = cudaStreamEndCapture(e->stream, &g);
+  if (r != cudaSuccess) return r;
+  if (r2 != cudaSuccess) return r2;
+  r = cudaGraphInstantiate(&e->graph[victim], g, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(g);
+  if (r != cudaSuccess) return r;
+  e->graph_len[victim] = len;
+  e->graph_use[victim] = e->graph_clock;
+  *out = e->graph[victim];
+  return cudaSuccess;
+}
+
 int set_device_m(cmc_engine* e, long m, cmc_error* err) {
   if (e->host_m == m) return CMC_OK;
   CUDA_TRY(cudaStreamSynchronize(e->stream));
@@ -1165,7 +1215,8 @@ int cmc_engine_destroy(cmc_engine* e) {
   if (e->dev_ready) {
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
-    if (e->graph) cudaGraphExecDestroy(e->graph);
+    for (auto& g : e->graph)
+      if (g) cudaGraphExecDestroy(g);
     DevBuf<double>* ds[] = {&e->y, &e->A, &e->Xd, &e->hd, &e->gval, &e->eps,
                             &e->eps_w, &e->eps_wa, &e->gam, &e->gam_w,
                             &e->gam_wa, &e->beta, &e->beta_w, &e->beta_wa,
@@ -1357,43 +1408,33 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
 #ifndef CMC_GRAPH_CHUNK
 #define CMC_GRAPH_CHUNK 50  // sweeps per CUDA graph (A/B: 25 0.3551 ms, 50 0.3531, 100 0.3527)
 #endif
-  const long chunk = CMC_GRAPH_CHUNK;
   CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
-  long done = 0;
-  if (total >= chunk && !e->loop) {
-    if (!e->graph || e->graph_len != chunk) {
-      if (e->graph) cudaGraphExecDestroy(e->graph);
-      e->graph = nullptr;
-      cudaGraph_t g;
-      CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-      // fork the other lanes and the tail streams into the capture
-      cudaError_t r = fork_lanes(e);
-      for (long off = 0; r == cudaSuccess && off < chunk; ++off)
-        r = enqueue_all_lanes(e, p, off);
-      if (r == cudaSuccess) r = join_lanes(e);
-      if (r == cudaSuccess) r = launch_advance(e->d_m.p, chunk, e->stream);
-      cudaError_t r2 = cudaStreamEndCapture(e->stream, &g);
-      CUDA_TRY(r);
-      CUDA_TRY(r2);
-      CUDA_TRY(cudaGraphInstantiate(&e->graph, g, cudaGraphInstantiateFlagUseNodePriority));
-      cudaGraphDestroy(g);
-      e->graph_len = chunk;
+  if (e->loop) {
+    // loopback group: eager launches (another engine's events cannot enter
+    // a capture)
+    CUDA_TRY(fork_lanes(e));
+    for (long off = 0; off < total; ++off) CUDA_TRY(enqueue_all_lanes(e, p, off));
+    CUDA_TRY(join_lanes(e));
+    CUDA_TRY(launch_advance(e->d_m.p, total, e->stream));
+  } else {
+    // whole 50-sweep graphs, then one graph of the remaining length: every
+    // sweep of the call replays from a graph (a 1-sweep call included)
+    const long chunk = CMC_GRAPH_CHUNK;
+    const long full = total / chunk, rest = total % chunk;
+    if (full) {
+      cudaGraphExec_t g = nullptr;
+      CUDA_TRY(sweep_graph(e, p, chunk, &g));
+      for (long k = 0; k < full; ++k) CUDA_TRY(cudaGraphLaunch(g, e->stream));
     }
-    for (; done + chunk <= total; done += chunk)
-      CUDA_TRY(cudaGraphLaunch(e->graph, e->stream));
-    // events recorded inside the capture cannot be waited on outside it:
+    if (rest) {
+      cudaGraphExec_t g = nullptr;
+      CUDA_TRY(sweep_graph(e, p, rest, &g));
+      CUDA_TRY(cudaGraphLaunch(g, e->stream));
+    }
+    // events recorded inside a capture cannot be waited on outside it:
     // re-arm them on the real streams (all work so far is stream-ordered)
     CUDA_TRY(fork_lanes(e));
     CUDA_TRY(join_lanes(e));
-  }
-  const long rest = total - done;
-  if (rest) {
-    // events recorded inside a capture cannot be waited on outside it:
-    // fork_lanes re-arms every event on the real streams
-    CUDA_TRY(fork_lanes(e));
-    for (long off = 0; off < rest; ++off) CUDA_TRY(enqueue_all_lanes(e, p, off));
-    CUDA_TRY(join_lanes(e));
-    CUDA_TRY(launch_advance(e->d_m.p, rest, e->stream));
   }
   CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
   e->timing_pending = true;
@@ -1444,10 +1485,19 @@ int cmc_engine_launches_per_sweep(const cmc_engine* e) {
   return n * std::max(1, e->n_lanes);
 }
 
-int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
-                       double* tail_ms, cmc_error* err) {
-  if (!e || reps < 1 || !e->begun) {
-    set_err(err, CMC_ERR_ARG, "profile needs begin() and reps >= 1");
+// Per-phase device time of `reps` further monitored sweeps of every chain
+// (one launch per phase for all chains, serialised on the engine stream,
+// CUDA events between phases).  ms[CMC_PHASES]: eps (step 1), gene (steps
+// 2 + 5), xi, leaf_a (+ nu, tau, theta), leaf_b (+ sigma, monitors),
+// gene_contrast; averages per sweep.
+int cmc_engine_profile_phases(cmc_engine* e, long m_begin, long reps, double* ms,
+                              cmc_error* err) {
+  if (!e || reps < 1 || !e->begun || !ms) {
+    set_err(err, CMC_ERR_ARG, "profile needs begin(), reps >= 1 and an output array");
+    return CMC_ERR_ARG;
+  }
+  if (e->split_tail) {
+    set_err(err, CMC_ERR_ARG, "profile is single-GPU only");
     return CMC_ERR_ARG;
   }
   CUDA_TRY(cudaSetDevice(e->device));
@@ -1457,42 +1507,48 @@ int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
   p.slot_base = 0;
   p.chain_base = 0;
   p.monitor_enabled = 1;
-  std::vector<cudaEvent_t> ev((size_t)(3 * reps));
+  constexpr int P = CMC_PHASES;
+  std::vector<cudaEvent_t> ev((size_t)((P + 1) * reps));
   for (auto& x : ev) CUDA_TRY(cudaEventCreate(&x));
+  cudaStream_t s = e->stream;
   for (long r = 0; r < reps; ++r) {
-    CUDA_TRY(cudaEventRecord(ev[3 * r], e->stream));
-    CUDA_TRY(launch_eps_sweep(p, e->C, r, e->stream));
-    CUDA_TRY(launch_gene_sweep(p, e->C, r, e->stream));
-    if (e->xi_any) CUDA_TRY(launch_xi_sweep(p, e->C, r, e->stream));
-    CUDA_TRY(cudaEventRecord(ev[3 * r + 1], e->stream));
-    SweepParams q = p;
-    // the tail: everything enqueue_sweep launches after the gene kernel
-    if (!e->split_tail) {
-      CUDA_TRY(launch_leaf_a(q, e->C, r, e->stream));
-      CUDA_TRY(launch_leaf_b(q, e->C, r, e->stream));
-    } else {
-      set_err(err, CMC_ERR_ARG, "profile is single-GPU only");
-      return CMC_ERR_ARG;
-    }
-    if (e->has_ctab && e->ctab.gene_needs_hyper)
-      CUDA_TRY(launch_gene_contrast(q, e->C, r, e->stream));
-    CUDA_TRY(cudaEventRecord(ev[3 * r + 2], e->stream));
+    cudaEvent_t* E = ev.data() + (P + 1) * r;
+    CUDA_TRY(cudaEventRecord(E[0], s));
+    CUDA_TRY(launch_eps_sweep(p, e->C, r, s));
+    CUDA_TRY(cudaEventRecord(E[1], s));
+    CUDA_TRY(launch_gene_sweep(p, e->C, r, s));
+    CUDA_TRY(cudaEventRecord(E[2], s));
+    if (e->xi_any) CUDA_TRY(launch_xi_sweep(p, e->C, r, s));
+    CUDA_TRY(cudaEventRecord(E[3], s));
+    CUDA_TRY(launch_leaf_a(p, e->C, r, s));
+    CUDA_TRY(cudaEventRecord(E[4], s));
+    CUDA_TRY(launch_leaf_b(p, e->C, r, s));
+    CUDA_TRY(cudaEventRecord(E[5], s));
+    if (e->has_ctab && e->ctab.gene_needs_hyper) CUDA_TRY(launch_gene_contrast(p, e->C, r, s));
+    CUDA_TRY(cudaEventRecord(E[6], s));
   }
-  CUDA_TRY(launch_advance(e->d_m.p, reps, e->stream));
-  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  CUDA_TRY(launch_advance(e->d_m.p, reps, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
   e->host_m = m_begin + reps;
-  double g = 0, t = 0;
-  for (long r = 0; r < reps; ++r) {
-    float a = 0, b = 0;
-    CUDA_TRY(cudaEventElapsedTime(&a, ev[3 * r], ev[3 * r + 1]));
-    CUDA_TRY(cudaEventElapsedTime(&b, ev[3 * r + 1], ev[3 * r + 2]));
-    g += a;
-    t += b;
-  }
+  for (int k = 0; k < P; ++k) ms[k] = 0.0;
+  for (long r = 0; r < reps; ++r)
+    for (int k = 0; k < P; ++k) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, ev[(P + 1) * r + k], ev[(P + 1) * r + k + 1]));
+      ms[k] += t / reps;
+    }
   for (auto& x : ev) cudaEventDestroy(x);
-  if (gene_ms) *gene_ms = g / reps;
-  if (tail_ms) *tail_ms = t / reps;
   return check_stall(e, 0, e->C, err);
+}
+
+int cmc_engine_profile(cmc_engine* e, long m_begin, long reps, double* gene_ms,
+                       double* tail_ms, cmc_error* err) {
+  double ms[CMC_PHASES];
+  const int rc = cmc_engine_profile_phases(e, m_begin, reps, ms, err);
+  if (rc) return rc;
+  if (gene_ms) *gene_ms = ms[0] + ms[1] + ms[2];
+  if (tail_ms) *tail_ms = ms[3] + ms[4] + ms[5];
+  return CMC_OK;
 }
 
 // Runs the diagnostics kernels over the resident accumulators and copies
@@ -2007,36 +2063,17 @@ int cmc_engine_shard_loopback(cmc_engine* e, int rank, cmc_loopback* g, cmc_erro
 // ------------------------------------------------------- synthetic inputs
 
 namespace {
-// Poisson(lambda) from the stream: inversion for small means, Hoermann's
-// PTRS transformed rejection for large ones.
-long long poisson_draw(Stream& s, double lam) {
-  if (lam < 10.0) {
-    const double L = std::exp(-lam);
-    long long k = 0;
-    double p = s.u01();
-    while (p > L) {
-      ++k;
-      p *= s.u01();
-    }
-    return k;
-  }
-  const double slam = std::sqrt(lam), loglam = std::log(lam);
-  const double b = 0.931 + 2.53 * slam;
-  const double a = -0.059 + 0.02483 * b;
-  const double inv_alpha = 1.1239 + 1.1328 / (b - 3.4);
-  const double vr = 0.9277 - 3.6224 / (b - 2.0);
-  for (;;) {
-    const double U = s.u01() - 0.5;
-    const double V = s.u01();
-    const double us = 0.5 - std::fabs(U);
-    const long long k = (long long)std::floor((2.0 * a / us + b) * U + lam + 0.43);
-    if (us >= 0.07 && V <= vr) return k;
-    if (k < 0 || (us < 0.013 && V > us)) continue;
-    if (std::log(V) + std::log(inv_alpha) - std::log(a / (us * us) + b) <=
-        -lam + (double)k * loglam - std::lgamma((double)k + 1.0))
-      return k;
-  }
-}
+// The reference draws counts with std::poisson_distribution<long long> over
+// its RngStream (P:src/simulate.cpp:82-83); Stream is the same Philox
+// stream, so the same standard-library distribution over it gives the
+// reference's counts bit for bit (same libstdc++ and glibc libm).
+struct StreamUrbg {
+  using result_type = uint64_t;
+  Stream* s;
+  static constexpr result_type min() { return 0; }
+  static constexpr result_type max() { return ~0ull; }
+  result_type operator()() { return s->next(); }
+};
 }  // namespace
 
 int cmc_simulate(long G, long N, long L, const double* X, const double* h,
@@ -2064,15 +2101,29 @@ int cmc_simulate(long G, long N, long L, const double* X, const double* h,
       double eta = 0.0;
       for (long l = 0; l < L; ++l) eta += X[n * L + l] * beta[l];
       const double arg = (h ? h[n] : 0.0) + e + eta;
-      if (arg > 700.0 || std::exp(arg) > 1e15) {
+      // SimulationError cases, P:src/simulate.cpp:64-81
+      if (arg > 700.0) {
         char buf[160];
         std::snprintf(buf, sizeof(buf),
-                      "simulated Poisson mean overflow at gene %ld, sample %ld", g + 1,
-                      n + 1);
+                      "simulated Poisson mean overflow at gene %ld, sample %ld "
+                      "(log mean %.6g exceeds %.0f)",
+                      g + 1, n + 1, arg, 700.0);
         set_err(err, CMC_ERR_CONFIG, buf);
         return CMC_ERR_CONFIG;
       }
-      counts[g * N + n] = poisson_draw(rng, std::exp(arg));
+      const double lambda = std::exp(arg);
+      if (lambda > 1e15) {
+        char buf[160];
+        std::snprintf(buf, sizeof(buf),
+                      "simulated Poisson mean %.6g at gene %ld, sample %ld is "
+                      "too large for integer counts",
+                      lambda, g + 1, n + 1);
+        set_err(err, CMC_ERR_CONFIG, buf);
+        return CMC_ERR_CONFIG;
+      }
+      std::poisson_distribution<long long> pois(lambda);
+      StreamUrbg u{&rng};
+      counts[g * N + n] = pois(u);
     }
   }
   return CMC_OK;

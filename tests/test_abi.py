@@ -138,3 +138,35 @@ def test_sample_count_beyond_gene_kernel_shared_memory():
     X = builtin_design("heterosis16x5", 224)   # fits
     GibbsEngine(CountMatrix(np.ones((8, 224), np.int64)), ModelSpec(X, np.zeros(224)),
                 RunConfig(chains=1, burnin=10, iterations=10))
+
+
+@pytest.mark.parametrize("G,N,seed,nu,tau,theta", [
+    (2000, 16, 1, 8.0, 0.7, [2.5, .2, .2, 0.0, .1]),    # the bench data (Paschold-shaped)
+    (400, 64, 1, 8.0, 0.7, [2.5, .2, .2, 0.0, .1]),     # config 5's N = 64 tiling
+    (300, 16, 9, 3.0, 0.5, [6.0, .5, .2, 0.0, .1]),     # large means: PTRD branch only
+    (300, 16, 4, 8.0, 0.7, [0.5, .2, .2, 0.0, .1]),     # small means: product branch
+])
+def test_simulate_equals_reference_generate(ref, G, N, seed, nu, tau, theta):
+    """cmc_simulate draws the reference's generate() (P:src/simulate.cpp:
+    28-90) bit for bit: same Philox site per gene, same normal/gamma draw
+    order, and std::poisson_distribution<long long> over the same stream, so
+    the bench's two arms consume identical arrays."""
+    import oracle
+    sigma = [.4, .25, .25, .15, .2]
+    X = builtin_design("heterosis16x5", N)
+    ours = generate(SimSpec(G=G, N=N, X=X, nu=nu, tau=tau, theta=theta, sigma=sigma,
+                            seed=seed)).counts
+    theirs, Xr = oracle.ref_generate(G, N, nu, tau, theta, sigma, seed)
+    assert np.array_equal(X, Xr)
+    assert np.array_equal(ours, theirs)
+
+
+def test_simulate_overflow_error_matches_reference(ref):
+    import oracle
+    X = builtin_design("heterosis16x5", 16)
+    kw = dict(nu=8.0, tau=0.7, theta=[800.0, 0, 0, 0, 0], sigma=[0.0] * 5, seed=1)
+    with pytest.raises(ConfigError) as ours:
+        generate(SimSpec(G=3, N=16, X=X, **kw))
+    with pytest.raises(oracle.ConfigErr) as theirs:
+        oracle.ref_generate(3, 16, kw["nu"], kw["tau"], kw["theta"], kw["sigma"], 1)
+    assert str(ours.value) == str(theirs.value)
