@@ -214,6 +214,10 @@ int cmc_engine_begin(cmc_engine* engine, cmc_error* err);
 int cmc_engine_sweeps(cmc_engine* engine, long m_begin, long m_end,
                       cmc_error* err);
 int cmc_engine_sync(cmc_engine* engine, cmc_error* err);
+/* Capture (and cache) the CUDA graphs a sweeps() call of `sweeps` sweeps
+ * replays, without running them: moves the one-time capture cost out of a
+ * timed region.  After begin(); no reference counterpart. */
+int cmc_engine_prepare(cmc_engine* engine, long sweeps, cmc_error* err);
 /* cudaStream_t the engine launches on (for event timing by the caller). */
 void* cmc_engine_stream(cmc_engine* engine);
 /* Kernel launches per sweep (gene kernel + hyper tail [+ contrast]). */
@@ -226,10 +230,12 @@ int cmc_engine_launches_per_sweep(const cmc_engine* engine);
 int cmc_engine_profile(cmc_engine* engine, long m_begin, long reps,
                        double* gene_ms, double* tail_ms, cmc_error* err);
 /* The same per sweep phase (single GPU): ms[CMC_PHASES] = average device ms
- * of eps (step 1), gene (steps 2 + 5), xi (extension), leaf_a (reductions
- * + nu, tau, theta: steps 3, 4, 6), leaf_b (reductions + sigma, step 7, and
- * the hyper monitors), gene_contrast; each phase one launch for all chains,
- * phases serialised with CUDA events between them. */
+ * of eps (step 1), gene (steps 2 + 5, and the leaf sums of steps 3/4/6
+ * without a xi prior), xi (extension), hyper_a (nu, tau, theta: steps 3, 4,
+ * 6; with a xi prior leaf_a, its leaf sums and those draws), leaf_b
+ * (reductions + sigma, step 7, and the hyper monitors), gene_contrast;
+ * each phase one launch for all chains, phases serialised with CUDA events
+ * between them. */
 #define CMC_PHASES 6
 int cmc_engine_profile_phases(cmc_engine* engine, long m_begin, long reps,
                               double* ms, cmc_error* err);

@@ -197,6 +197,7 @@ struct cmc_loopback {
   bool broken = false;  // a rank failed or timed out: every barrier fails
   std::vector<const double*> send;
   std::vector<cudaEvent_t> ready, copied;
+  std::vector<std::vector<double>> xrec;  // stall records per rank (sync)
   // false if the group is broken or a peer does not arrive within 120 s (a
   // rank that failed elsewhere never reaches its next exchange)
   bool barrier() {
@@ -278,6 +279,9 @@ struct cmc_engine {
   DevBuf<double> eps, eps_w, eps_wa, gam, gam_w, gam_wa, beta, beta_w, beta_wa;
   DevBuf<double> log_gam, inv_gam, acc_eps, acc_gam, acc_beta, cprob, samples;
   DevBuf<double> partA, partB;
+  DevBuf<unsigned int> leaf_cnt;  // [slots][local leaves]: gene blocks done per leaf
+  DevBuf<double> stall_x;         // sharded sync: [world][C][4] stall records
+  cudaEvent_t ev_coll = nullptr;  // last collective enqueued (any lane): one order
   DevBuf<double> xi, xi_w, xi_wa, acc_xi;  // [C][L][G] (acc: [C][4][L][G])
   DevBuf<double> xfer;  // max(N, L) x G: layout transposes for host transfers
   DevBuf<Hyper> hyper;
@@ -340,7 +344,20 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaEventCreate(&e->ev0));
   CUDA_TRY(cudaEventCreate(&e->ev1));
   const long G = e->G, N = e->N, L = e->L, C = e->C;
-  const int Q = 2 + (int)L + (e->xi_any ? (int)L : 0);
+  const int Qs = leaf_qs_a((int)L, e->xi_any ? 1 : 0);
+  {
+    // dynamic shared memory opt-in of the gene kernels on this device; the
+    // static part counts against the same per-block limit
+    int total = 0, optin = 0;
+    CUDA_TRY(configure_gene_kernels((int)N, e->Jmax, e->xi_any ? 1 : 0, &total));
+    CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    if (total > optin) {
+      set_err(err, CMC_ERR_CONFIG,
+              "N (plus 2x the groups per model-matrix column) too large for this build's gene "
+              "kernel shared memory");
+      return CMC_ERR_CONFIG;
+    }
+  }
   // SoA y[n][g] as double (exact for counts < 2^53)
   std::vector<double> yh((size_t)N * G);
   for (long g = 0; g < G; ++g)
@@ -415,7 +432,13 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(e->xfer.alloc((size_t)std::max(N, L) * G));
   const long n_leaves_total = (e->G_total + kLeaf - 1) / kLeaf;
   const long lpr = (n_leaves_total + e->world - 1) / e->world;
-  CUDA_TRY(e->partA.alloc((size_t)e->world * Cs * Q * lpr));
+  CUDA_TRY(e->partA.alloc((size_t)e->world * Cs * Qs * lpr));
+  CUDA_TRY(cudaMemset(e->partA.p, 0, sizeof(double) * e->partA.n));
+  const long n_leaves_local = (G + kLeaf - 1) / kLeaf;
+  CUDA_TRY(e->leaf_cnt.alloc((size_t)Cs * n_leaves_local));
+  CUDA_TRY(cudaMemset(e->leaf_cnt.p, 0, sizeof(unsigned int) * e->leaf_cnt.n));
+  if (e->world > 1) CUDA_TRY(e->stall_x.alloc((size_t)e->world * Cs * 4));
+  CUDA_TRY(cudaEventCreateWithFlags(&e->ev_coll, cudaEventDisableTiming));
   CUDA_TRY(e->partB.alloc((size_t)e->world * Cs * L * lpr));
   CUDA_TRY(e->dctab.alloc(1));
   CUDA_TRY(cudaMemcpy(e->dctab.p, &e->ctab, sizeof(ContrastTable),
@@ -438,6 +461,10 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.world = e->world;
   p.Jmax = e->Jmax;
   p.fuse_tail = e->split_tail ? 0 : 1;
+  // without a xi prior the gene kernel sums its own leaves (the xi sums
+  // need the xi kernel's draws: leaf_a kernel)
+  p.fuse_leaf_a = e->xi_any ? 0 : 1;
+  p.leaf_cnt = e->leaf_cnt.p;
   p.y = e->y.p;
   p.A = e->A.p;
   p.X = e->Xd.p;
@@ -664,7 +691,12 @@ int upload_state(cmc_engine* e, long c, const double* st, const double* tw,
   hp.err_key = kNoError;
   hp.err_key_eps = kNoError;
   hp.doneA = hp.doneB = 0;
+  hp.peer_stall = 0;
   CUDA_TRY(cudaMemcpy(e->hyper.p + c, &hp, sizeof(Hyper), cudaMemcpyHostToDevice));
+  // the per-leaf block counters of this slot (a stalled sweep may have left
+  // them mid-count)
+  const size_t nl = (size_t)((e->G + kLeaf - 1) / kLeaf);
+  CUDA_TRY(cudaMemset(e->leaf_cnt.p + (size_t)c * nl, 0, sizeof(unsigned int) * nl));
   return CMC_OK;
 }
 
@@ -717,58 +749,156 @@ int download_state(cmc_engine* e, long c, double* st, double* tw, double* ta,
   return CMC_OK;
 }
 
-// Decode the device stall record of the lowest stalled chain slot.
+// One chain's stall record on the host: iteration (-1: none), packed key
+// (sweep.h stall_key, global gene index), stalled value and width.
+struct StallRec {
+  long long m = -1;
+  unsigned long long key = kNoError;
+  double x0 = 0.0, w = 0.0;
+};
+
+// Decode slot c's device stall record (two slots, see sweep_kernels.cu
+// record_stall: the earlier iteration wins, then the smaller key, i.e. the
+// reference's sequential order).  A stalled step leaves its value and
+// width untouched on the device, where they are read back.
+cudaError_t local_stall(cmc_engine* e, long c, StallRec* out) {
+  Hyper hp;
+  cudaError_t r = cudaMemcpy(&hp, e->hyper.p + c, sizeof(Hyper), cudaMemcpyDeviceToHost);
+  if (r != cudaSuccess) return r;
+  *out = StallRec{};
+  if (hp.err_key == kNoError && hp.err_key_eps == kNoError) return cudaSuccess;
+  unsigned long long key = hp.err_key;
+  long long km = hp.err_m;
+  if (hp.err_key_eps != kNoError &&
+      (hp.err_key == kNoError || hp.err_m_eps < hp.err_m ||
+       (hp.err_m_eps == hp.err_m && hp.err_key_eps < hp.err_key))) {
+    key = hp.err_key_eps;
+    km = hp.err_m_eps;
+  }
+  const unsigned step = (unsigned)(key >> 60);
+  const long col = (long)((key >> 52) & 0xff);
+  const long g = (long)((key >> 20) & 0xffffffffull);
+  const long n = (long)(key & 0xfffff);
+  double x0 = 0, w = 0;
+  if (step == 1 || step == 2 || step == 5) {
+    const size_t gl = (size_t)(g - e->g0), G = (size_t)e->G;
+    // step 5 with n == 1 is xi_gl (extension), drawn right after beta_gl
+    const bool xs5 = step == 5 && n == 1;
+    const double* xs = step == 1 ? e->eps.p + (size_t)c * e->N * G + (size_t)n * G + gl
+                       : step == 2 ? e->gam.p + (size_t)c * G + gl
+                       : xs5       ? e->xi.p + (size_t)c * e->L * G + (size_t)col * G + gl
+                                   : e->beta.p + (size_t)c * e->L * G + (size_t)col * G + gl;
+    const double* ws = step == 1 ? e->eps_w.p + (size_t)c * e->N * G + (size_t)n * G + gl
+                       : step == 2 ? e->gam_w.p + (size_t)c * G + gl
+                       : xs5       ? e->xi_w.p + (size_t)c * e->L * G + (size_t)col * G + gl
+                                   : e->beta_w.p + (size_t)c * e->L * G + (size_t)col * G + gl;
+    if ((r = cudaMemcpy(&x0, xs, sizeof(double), cudaMemcpyDeviceToHost)) != cudaSuccess) return r;
+    if ((r = cudaMemcpy(&w, ws, sizeof(double), cudaMemcpyDeviceToHost)) != cudaSuccess) return r;
+  } else {
+    const int k = step == 3 ? 0 : step == 4 ? 1 : 2 + (int)col;
+    x0 = hp.err_x0[k];
+    w = hp.err_w[k];
+  }
+  *out = StallRec{km, key, x0, w};
+  return cudaSuccess;
+}
+
+void report_stall(const StallRec& s, cmc_error* err) {
+  const unsigned step = (unsigned)(s.key >> 60);
+  const long col = (long)((s.key >> 52) & 0xff);
+  const long g = (long)((s.key >> 20) & 0xffffffffull);
+  const long n = (long)(s.key & 0xfffff);
+  const long it = (long)s.m;
+  switch (step) {
+    case 1: set_stall(err, "epsilon", g + 1, n + 1, s.x0, s.w, it); break;
+    case 2: set_stall(err, "gamma", g + 1, -1, s.x0, s.w, it); break;
+    case 3: set_stall(err, "nu", -1, -1, s.x0, s.w, it); break;
+    case 4: set_stall(err, "tau", -1, -1, s.x0, s.w, it); break;
+    case 5: set_stall(err, n == 1 ? "xi" : "beta", g + 1, col + 1, s.x0, s.w, it); break;
+    default: set_stall(err, "sigma", col + 1, -1, s.x0, s.w, it); break;
+  }
+}
+
+// Sharded runs: every rank's records of slots [lo, hi) to every rank, so
+// all ranks raise the same SamplerStallError (a gene stall is recorded on
+// the owning rank only; its peers stopped the chain from the gathered
+// flags).  NCCL all-gather of [m, key bits, x0, w] per slot on the engine
+// stream, or the loopback group's host exchange.
+int exchange_stalls(cmc_engine* e, long lo, long hi, std::vector<StallRec>& recs,
+                    std::vector<StallRec>& all, cmc_error* err) {
+  const long n = hi - lo;
+  const int W = e->world;
+  all.assign((size_t)W * n, StallRec{});
+  std::vector<double> mine((size_t)n * 4), got((size_t)W * n * 4);
+  for (long i = 0; i < n; ++i) {
+    mine[4 * i] = (double)recs[i].m;
+    std::memcpy(&mine[4 * i + 1], &recs[i].key, 8);
+    mine[4 * i + 2] = recs[i].x0;
+    mine[4 * i + 3] = recs[i].w;
+  }
+  if (e->loop) {
+    cmc_loopback& g = *e->loop;
+    {
+      std::lock_guard<std::mutex> lk(g.mu);
+      if (g.xrec.size() < (size_t)W) g.xrec.resize((size_t)W);
+      g.xrec[(size_t)e->rank] = mine;
+    }
+    if (!g.barrier()) {
+      set_err(err, CMC_ERR_NCCL, "loopback group broken during the stall exchange");
+      return CMC_ERR_NCCL;
+    }
+    for (int r = 0; r < W; ++r)
+      std::copy(g.xrec[(size_t)r].begin(), g.xrec[(size_t)r].end(), got.begin() + (size_t)r * n * 4);
+    if (!g.barrier()) {
+      set_err(err, CMC_ERR_NCCL, "loopback group broken during the stall exchange");
+      return CMC_ERR_NCCL;
+    }
+  } else {
+    double* d = e->stall_x.p;
+    CUDA_TRY(cudaMemcpyAsync(d + (size_t)e->rank * n * 4, mine.data(), sizeof(double) * n * 4,
+                             cudaMemcpyHostToDevice, e->stream));
+    if (g_nccl.all_gather(d + (size_t)e->rank * n * 4, d, (size_t)n * 4, kNcclFloat64, e->comm,
+                          e->stream) != 0) {
+      set_err(err, CMC_ERR_NCCL, "ncclAllGather of the stall records failed");
+      return CMC_ERR_NCCL;
+    }
+    CUDA_TRY(cudaMemcpyAsync(got.data(), d, sizeof(double) * W * n * 4, cudaMemcpyDeviceToHost,
+                             e->stream));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+  }
+  for (size_t i = 0; i < all.size(); ++i) {
+    all[i].m = (long long)got[4 * i];
+    std::memcpy(&all[i].key, &got[4 * i + 1], 8);
+    all[i].x0 = got[4 * i + 2];
+    all[i].w = got[4 * i + 3];
+  }
+  return CMC_OK;
+}
+
+// The stall to report for slots [lo, hi): the lowest stalled chain (the
+// reference runs chains in order), and within it the earliest iteration,
+// then the smallest key, over every rank.
 int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
-  for (long c = slot_lo; c < slot_hi; ++c) {
-    Hyper hp;
-    CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + c, sizeof(Hyper), cudaMemcpyDeviceToHost));
-    if (hp.err_key == kNoError && hp.err_key_eps == kNoError) continue;
-    // two slots (see sweep_kernels.cu record_stall): the earlier iteration
-    // wins, then the smaller key (the reference's sequential order)
-    unsigned long long key = hp.err_key;
-    long long km = hp.err_m;
-    if (hp.err_key_eps != kNoError &&
-        (hp.err_key == kNoError || hp.err_m_eps < hp.err_m ||
-         (hp.err_m_eps == hp.err_m && hp.err_key_eps < hp.err_key))) {
-      key = hp.err_key_eps;
-      km = hp.err_m_eps;
+  const long n = slot_hi - slot_lo;
+  std::vector<StallRec> recs((size_t)n);
+  for (long c = slot_lo; c < slot_hi; ++c) CUDA_TRY(local_stall(e, c, &recs[(size_t)(c - slot_lo)]));
+  std::vector<StallRec> all = recs;
+  if (e->world > 1) {
+    const int rc = exchange_stalls(e, slot_lo, slot_hi, recs, all, err);
+    if (rc) return rc;
+  }
+  const int W = e->world > 1 ? e->world : 1;
+  for (long i = 0; i < n; ++i) {
+    const StallRec* best = nullptr;
+    for (int r = 0; r < W; ++r) {
+      const StallRec& s = all[(size_t)r * n + i];
+      if (s.m < 0) continue;
+      if (!best || s.m < best->m || (s.m == best->m && s.key < best->key)) best = &s;
     }
-    hp.err_m = km;
-    const unsigned step = (unsigned)(key >> 60);
-    const long col = (long)((key >> 52) & 0xff);
-    const long g = (long)((key >> 20) & 0xffffffffull);
-    const long n = (long)(key & 0xfffff);
-    double x0 = 0, w = 0;
-    if (step == 1 || step == 2 || step == 5) {
-      // a stalled step leaves its value and width untouched on the device
-      const size_t gl = (size_t)(g - e->g0), G = (size_t)e->G;
-      // step 5 with n == 1 is xi_gl (extension), drawn right after beta_gl
-      const bool xs5 = step == 5 && n == 1;
-      const double* xs = step == 1 ? e->eps.p + (size_t)c * e->N * G + (size_t)n * G + gl
-                         : step == 2 ? e->gam.p + (size_t)c * G + gl
-                         : xs5       ? e->xi.p + (size_t)c * e->L * G + (size_t)col * G + gl
-                                     : e->beta.p + (size_t)c * e->L * G + (size_t)col * G + gl;
-      const double* ws = step == 1 ? e->eps_w.p + (size_t)c * e->N * G + (size_t)n * G + gl
-                         : step == 2 ? e->gam_w.p + (size_t)c * G + gl
-                         : xs5       ? e->xi_w.p + (size_t)c * e->L * G + (size_t)col * G + gl
-                                     : e->beta_w.p + (size_t)c * e->L * G + (size_t)col * G + gl;
-      CUDA_TRY(cudaMemcpy(&x0, xs, sizeof(double), cudaMemcpyDeviceToHost));
-      CUDA_TRY(cudaMemcpy(&w, ws, sizeof(double), cudaMemcpyDeviceToHost));
-    } else {
-      const int k = step == 3 ? 0 : step == 4 ? 1 : 2 + (int)col;
-      x0 = hp.err_x0[k];
-      w = hp.err_w[k];
+    if (best) {
+      report_stall(*best, err);
+      return CMC_ERR_STALL;
     }
-    const long it = (long)hp.err_m;
-    switch (step) {
-      case 1: set_stall(err, "epsilon", g + 1, n + 1, x0, w, it); break;
-      case 2: set_stall(err, "gamma", g + 1, -1, x0, w, it); break;
-      case 3: set_stall(err, "nu", -1, -1, x0, w, it); break;
-      case 4: set_stall(err, "tau", -1, -1, x0, w, it); break;
-      case 5: set_stall(err, n == 1 ? "xi" : "beta", g + 1, col + 1, x0, w, it); break;
-      default: set_stall(err, "sigma", col + 1, -1, x0, w, it); break;
-    }
-    return CMC_ERR_STALL;
   }
   return CMC_OK;
 }
@@ -838,38 +968,47 @@ cudaError_t enqueue_sweep_on(cmc_engine* e, const SweepParams& p_in, int chains,
                              cudaEvent_t ev_gene, cudaEvent_t ev_tail,
                              nccl_comm comm) {
   // this launch's chains own a contiguous section of the partial buffers:
-  // [world][chains][Q][lpr] at world * slot_base * Q * lpr
+  // [world][chains][Qs][lpr] at world * slot_base * Qs * lpr
   SweepParams p = p_in;
-  const int Q = leaf_q_a((int)e->L, e->xi_any ? 1 : 0);
+  const int Qs = leaf_qs_a((int)e->L, e->xi_any ? 1 : 0);
   const size_t lpr = (size_t)p.leaves_per_rank, W = (size_t)e->world;
-#ifndef CMC_BISECT_NOOFF
-  p.partA = e->partA.p + W * (size_t)p.slot_base * Q * lpr;
+  p.partA = e->partA.p + W * (size_t)p.slot_base * Qs * lpr;
   p.partB = e->partB.p + W * (size_t)p.slot_base * e->L * lpr;
   p.C = chains;
-#endif
   DBG_SYNC("enter");
   cudaError_t r = launch_eps_sweep(p, chains, off, s);
   if (r != cudaSuccess) return r;
   DBG_SYNC("eps");
   if ((r = cudaStreamWaitEvent(s, ev_tail, 0)) != cudaSuccess) return r;
+  // gene kernel: steps 2 and 5 and, without a xi prior, the leaf sums of
+  // steps 3/4/6 and (one GPU) the nu, tau, theta draws themselves
   if ((r = launch_gene_sweep(p, chains, off, s)) != cudaSuccess) return r;
   DBG_SYNC("gene");
   if (e->xi_any && (r = launch_xi_sweep(p, chains, off, s)) != cudaSuccess) return r;
   if ((r = cudaEventRecord(ev_gene, s)) != cudaSuccess) return r;
   if ((r = cudaStreamWaitEvent(t, ev_gene, 0)) != cudaSuccess) return r;
+  if (!p.fuse_leaf_a && (r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
+  DBG_SYNC("leaf_a");
   if (!e->split_tail) {
-    if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
-    DBG_SYNC("leaf_a");
+    // one GPU: leaf_a's last block runs nu/tau/theta; after the gene
+    // kernel's fused leaf sums, hyper_a does
+    if (p.fuse_leaf_a && (r = launch_hyper_a(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
     DBG_SYNC("leaf_b");
   } else {
-    const size_t cA = (size_t)chains * Q * lpr;
+    // Every collective of every lane is ordered after the previously
+    // enqueued one (ev_coll), so all ranks issue them in one order: lane 0
+    // A, lane 0 B, lane 1 A, lane 1 B, then the next sweep.  Communicators
+    // of different lanes can then never wait on each other in different
+    // orders on different ranks.
+    const size_t cA = (size_t)chains * Qs * lpr;
     const size_t cB = (size_t)chains * e->L * lpr;
-    if ((r = launch_leaf_a(p, chains, off, t)) != cudaSuccess) return r;
+    if ((r = cudaStreamWaitEvent(t, e->ev_coll, 0)) != cudaSuccess) return r;
     if ((r = all_gather_parts(e, p.partA, cA, comm, t)) != cudaSuccess) return r;
     if ((r = launch_hyper_a(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = launch_leaf_b(p, chains, off, t)) != cudaSuccess) return r;
     if ((r = all_gather_parts(e, p.partB, cB, comm, t)) != cudaSuccess) return r;
+    if ((r = cudaEventRecord(e->ev_coll, t)) != cudaSuccess) return r;
     if ((r = launch_hyper_b(p, chains, off, t)) != cudaSuccess) return r;
   }
   if (p.monitor_enabled && e->has_ctab && e->ctab.gene_needs_hyper)
@@ -899,6 +1038,9 @@ cudaError_t fork_lanes(cmc_engine* e) {
     if ((r = cudaStreamWaitEvent(ln.s, e->ev_fork, 0)) != cudaSuccess) return r;
     if ((r = cudaEventRecord(ln.ev_tail, ln.s)) != cudaSuccess) return r;
   }
+  // the collective-order event too (captures may only wait on events
+  // recorded inside them)
+  if (e->ev_coll && (r = cudaEventRecord(e->ev_coll, e->stream)) != cudaSuccess) return r;
   return cudaEventRecord(e->ev_tail, e->stream);
 }
 
@@ -1118,11 +1260,13 @@ int cmc_engine_create(const cmc_problem* p, const cmc_run_config* config,
   {
     // the gene kernel keeps lp (N) and, beyond 2 groups per column, the
     // group sums (2 Jmax) per gene in shared memory
+    // (1 KB reserved for the kernel's static shared memory; ensure_device
+    // checks the exact total against the device's opt-in limit)
     const int smem = gene_sweep_smem_bytes((int)p->N, jmax <= 2 ? 0 : jmax);
-    if (smem > 227 * 1024) {
+    if (smem + 1024 > 227 * 1024) {
       delete e;
       return fail_config(err, "N (plus 2x the groups per model-matrix column) too large for "
-                              "this build's gene kernel: at most 227 samples");
+                              "this build's gene kernel: at most 226 samples");
     }
   }
 
@@ -1229,6 +1373,9 @@ int cmc_engine_destroy(cmc_engine* e) {
     e->gmem.free_();
     e->saved_slot.free_();
     e->hyper.free_();
+    e->leaf_cnt.free_();
+    e->stall_x.free_();
+    if (e->ev_coll) cudaEventDestroy(e->ev_coll);
     e->dctab.free_();
     e->d_m.free_();
     if (e->ev0) cudaEventDestroy(e->ev0);
@@ -1340,6 +1487,9 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
   const unsigned long long before = hp.clamps;
   hp.err_key = kNoError;
   hp.err_key_eps = kNoError;
+  hp.peer_stall = 0;
+  CUDA_TRY(cudaMemcpy(&e->hyper.p[slot].peer_stall, &hp.peer_stall, sizeof(unsigned int),
+                      cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(&e->hyper.p[slot].err_key, &hp.err_key,
                       sizeof(unsigned long long), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(&e->hyper.p[slot].err_key_eps, &hp.err_key_eps,
@@ -1354,7 +1504,8 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
   CUDA_TRY(cudaMemcpy(&hp, e->hyper.p + slot, sizeof(Hyper), cudaMemcpyDeviceToHost));
   if (clamps) *clamps += hp.clamps - before;
   if ((rc = set_device_m(e, run_m, err))) return rc;
-  if (hp.err_key != kNoError || hp.err_key_eps != kNoError)
+  // sharded: every rank takes part in the record exchange, stalled or not
+  if (e->world > 1 || hp.err_key != kNoError || hp.err_key_eps != kNoError)
     return check_stall(e, slot, slot + 1, err);
   return CMC_OK;
 }
@@ -1442,6 +1593,23 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
   return CMC_OK;
 }
 
+int cmc_engine_prepare(cmc_engine* e, long sweeps, cmc_error* err) {
+  if (!e || sweeps < 1 || !e->begun) {
+    set_err(err, CMC_ERR_ARG, "prepare needs begin() and sweeps >= 1");
+    return CMC_ERR_ARG;
+  }
+  if (e->loop) return CMC_OK;  // loopback sweeps are eager
+  CUDA_TRY(cudaSetDevice(e->device));
+  SweepParams p = e->base;
+  p.slot_base = 0;
+  p.chain_base = 0;
+  p.monitor_enabled = 1;
+  cudaGraphExec_t g = nullptr;
+  if (sweeps >= CMC_GRAPH_CHUNK) CUDA_TRY(sweep_graph(e, p, CMC_GRAPH_CHUNK, &g));
+  if (sweeps % CMC_GRAPH_CHUNK) CUDA_TRY(sweep_graph(e, p, sweeps % CMC_GRAPH_CHUNK, &g));
+  return CMC_OK;
+}
+
 int cmc_engine_sync(cmc_engine* e, cmc_error* err) {
   if (!e) return CMC_ERR_ARG;
   if (!e->dev_ready) return CMC_OK;
@@ -1478,9 +1646,12 @@ void* cmc_engine_stream(cmc_engine* e) {
 
 int cmc_engine_launches_per_sweep(const cmc_engine* e) {
   if (!e) return 0;
-  // per lane: eps, gene, [xi], leaf_a, leaf_b (+ hyper_a/b when split)
-  int n = e->split_tail ? 6 : 4;
-  if (e->xi_any) ++n;
+  // per lane: eps, gene (+ its fused leaf sums), hyper_a (nu, tau, theta),
+  // leaf_b (+ sigma); a xi prior: + xi, and leaf_a replaces the fused sums
+  // (its last block draws nu/tau/theta on one GPU); sharded: + hyper_b
+  int n = 4;
+  if (e->xi_any) n += e->split_tail ? 2 : 1;
+  if (e->split_tail) ++n;
   if (e->has_ctab && e->ctab.gene_needs_hyper) ++n;
   return n * std::max(1, e->n_lanes);
 }
@@ -1520,7 +1691,7 @@ int cmc_engine_profile_phases(cmc_engine* e, long m_begin, long reps, double* ms
     CUDA_TRY(cudaEventRecord(E[2], s));
     if (e->xi_any) CUDA_TRY(launch_xi_sweep(p, e->C, r, s));
     CUDA_TRY(cudaEventRecord(E[3], s));
-    CUDA_TRY(launch_leaf_a(p, e->C, r, s));
+    CUDA_TRY(p.fuse_leaf_a ? launch_hyper_a(p, e->C, r, s) : launch_leaf_a(p, e->C, r, s));
     CUDA_TRY(cudaEventRecord(E[4], s));
     CUDA_TRY(launch_leaf_b(p, e->C, r, s));
     CUDA_TRY(cudaEventRecord(E[5], s));

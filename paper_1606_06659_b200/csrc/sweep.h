@@ -59,6 +59,10 @@ struct Hyper {
   unsigned long long err_key_eps;  // stall slot of the eps kernel
   long long err_m_eps;
   unsigned int doneA, doneB;  // last-block counters of the two leaf phases
+  // sharded runs: another rank's chain stalled (seen in the gathered stall
+  // flags); this rank's kernels of the chain stop, and sync reports the
+  // stalling rank's record (exchanged across ranks)
+  unsigned int peer_stall;
 };
 
 struct ContrastTable {
@@ -87,6 +91,8 @@ struct SweepParams {
   int world;
   int Jmax;
   int fuse_tail;  // single GPU: the last leaf block runs the hyper step
+  int fuse_leaf_a;  // the gene kernel's last block per leaf sums it (no xi prior)
+  unsigned int* leaf_cnt;  // [slots][n_leaves_local] finished gene blocks per leaf
   const double* y;  // [N][G]
   const double* A;  // [L][G]
   const double* X;  // [N*L] row-major
@@ -125,7 +131,7 @@ struct SweepParams {
   // Leaf partials of THIS launch's chains (one lane): [world][C][Q][lpr]
   // and [world][C][L][lpr], indexed by slot - slot_base, so each lane's
   // block is contiguous per rank and one all-gather moves it.
-  double* partA;  // Q = leaf_q_a(L, xi_any)
+  double* partA;  // quantity stride leaf_qs_a(L, xi_any): Q sums + the stall flag
   double* partB;
   int C;          // chains of this launch's lane (stride of the partial buffers)
   // optional block timeline (debug/profiling): per record {kernel<<56 |
@@ -149,6 +155,11 @@ struct SweepParams {
 
 // leaf quantities of partA
 __host__ __device__ inline int leaf_q_a(int L, int xi_any) { return 2 + L + (xi_any ? L : 0); }
+// quantity stride of partA: the Q sums, then this rank's stall flag of the
+// chain at leaf slot 0 (gathered with the sums, read by hyper_a)
+__host__ __device__ inline int leaf_qs_a(int L, int xi_any) { return leaf_q_a(L, xi_any) + 1; }
+constexpr int kBlocksPerLeaf = kLeaf / kGeneThreads;  // gene blocks per reduction leaf
+constexpr int kStage = 128;  // values per warp per staging round of the serial leaf sums
 
 // Launch wrappers (sweep_kernels.cu).  `chains` = grid.y.
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
@@ -172,6 +183,11 @@ cudaError_t launch_fastmath_setup(cudaStream_t s);
 cudaError_t launch_compute_A(const double* y, const double* X, double* A,
                              int G, int N, int L, cudaStream_t s);
 int gene_sweep_smem_bytes(int N, int Jmax);
+// Raise the dynamic shared-memory opt-in of the gene kernel variant for
+// (N, Jmax, xi) on the current device (never lowers it: engines of one
+// process may share a device); *total = its static + dynamic bytes per
+// block, compared by the caller with the device's opt-in limit.
+cudaError_t configure_gene_kernels(int N, int Jmax, int xi_any, int* total);
 // [K][G] <-> [G][K] (to_aos: SoA -> AoS) on the device
 cudaError_t launch_transpose(const double* src, double* dst, long G, int K, bool to_aos,
                              cudaStream_t s);

@@ -26,7 +26,9 @@
 
 #include "fastmath.cuh"
 #include "rng.cuh"
+#include <algorithm>
 #include <cassert>
+#include <mutex>
 #include <type_traits>
 
 #include "sweep.h"
@@ -428,7 +430,19 @@ __device__ __forceinline__ void moments(double* acc, size_t stride, double v,
 // may overlap the previous iteration's tail; the host reports the record
 // with the smaller (iteration, key).
 __device__ __forceinline__ bool stalled_chain(const Hyper* hp) {
-  return hp->err_key != kNoError || hp->err_key_eps != kNoError;
+  return hp->err_key != kNoError || hp->err_key_eps != kNoError || hp->peer_stall;
+}
+
+// The same test for the tail of iteration m (leaf sums, hyper draws): the
+// eps kernel of iteration m + 1 runs beside it, and its stall must not stop
+// iteration m's tail (the reference draws nu..sigma of m before eps of
+// m + 1).  The eps kernel writes err_m_eps before its key (release), so a
+// key seen here has its iteration readable after a fence.
+__device__ __forceinline__ bool tail_stalled(const Hyper* hp, long m) {
+  if (hp->err_key != kNoError || hp->peer_stall) return true;
+  if (*(volatile const unsigned long long*)&hp->err_key_eps == kNoError) return false;
+  __threadfence();
+  return *(volatile const long long*)&hp->err_m_eps <= m;
 }
 
 __device__ __forceinline__ void record_stall(Hyper* hp, unsigned long long key,
@@ -573,8 +587,11 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
     // eps and its width stay untouched: the host reads x0 and w back.
     // The eps kernel of iteration m+1 runs concurrently with the tail of
     // iteration m, so it records into its own slot (see stalled_chain).
+    // the iteration first, then the key (see tail_stalled); every stalling
+    // lane of one kernel writes the same m
+    *(volatile long long*)&hp->err_m_eps = m;
+    __threadfence();
     atomicMin(&hp->err_key_eps, stall_key(1, 0, gg, n));
-    hp->err_m_eps = m;
   } else {
     p.eps[ie] = x1;
     if (tuning) {
@@ -600,13 +617,8 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 // XI: some column has a xi prior (extension); the reference model (all
 // normal) is compiled without the xi step.
 template <int JR, bool XI>
-__global__ void __launch_bounds__(kGeneThreads, CMC_GENE_MIN_BLOCKS)
-    gene_sweep_kernel(const SweepParams p, const long m_off) {
-  extern __shared__ double smem[];
-  __shared__ double exp_tab[32];
-  exp_table_init(exp_tab);
-  __syncthreads();
-  const ExpTab etab(exp_tab);
+__device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long m_off,
+                                                double* smem, const ExpTab etab) {
   WarpTrace wt(p, 2, p.slot_base + blockIdx.y);
   const int tid = threadIdx.x;
   const int slot = p.slot_base + blockIdx.y;
@@ -816,6 +828,7 @@ __global__ void __launch_bounds__(kGeneThreads, CMC_GENE_MIN_BLOCKS)
   if (clamps) atomicAdd(&hp->clamps, (unsigned long long)clamps);
 }
 
+
 // xi_gl for every (gene, xi column) of the chain (extension, no reference:
 // parity unpinned).  xi_gl's conditional reads only beta_gl (this sweep),
 // theta_l and sigma_l (iteration m-1), so all G x L steps are independent:
@@ -869,46 +882,70 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_MIN_BLOCKS)
             (double)(m - p.burnin));
 }
 
-// Serial sum of one 1024-gene leaf by one warp, in gene order: every lane
-// carries the same running sum; the leaf's 1024 values are loaded up front
-// (32 independent coalesced loads per lane) and broadcast lane by lane, so
-// the only dependent chain is the reference's left-to-right leaf loop
-// (P:include/countmc/parallel.hpp:76-81).
+// Serial sum of value(i), i in [start, end), from +0.0 in index order: the
+// reference's left-to-right leaf loop (P:include/countmc/parallel.hpp:
+// 76-81).  The warp stages kStage values at a time in its shared buffer
+// (coalesced loads, the next chunk in flight while this one is summed) and
+// lane 0 adds them one by one from shared memory, so the dependent chain is
+// one DADD per value with nothing else on it.  Padding past `end` with +0.0
+// is exact: the running sum starts at +0.0 and can never become -0.0, so
+// s + 0.0 == s.  Called by a whole warp; every lane gets the sum.
 template <class V>
-__device__ __forceinline__ double warp_leaf_sum(V value, long start, long end) {
+__device__ __forceinline__ double warp_serial_sum(V value, long start, long end, double* buf) {
   const int lane = threadIdx.x & 31;
-  const long n = end - start;
-  double v[32];
+  constexpr int PER = kStage / 32;
+  const int chunks = (int)((end - start + kStage - 1) / kStage);
+  double v[PER];
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    const long idx = start + c * 32 + lane;
-    v[c] = idx < end ? value(idx) : 0.0;
+  for (int k = 0; k < PER; ++k) {
+    const long idx = start + k * 32 + lane;
+    v[k] = idx < end ? value(idx) : 0.0;
   }
-  // Padding past the leaf end with +0.0 is exact: the running sum starts at
-  // +0.0 and can never become -0.0, so s + 0.0 == s.
-  (void)n;
   double s = 0.0;
+  for (int c = 0; c < chunks; ++c) {
 #pragma unroll
-  for (int c = 0; c < 32; ++c) {
+    for (int k = 0; k < PER; ++k) buf[k * 32 + lane] = v[k];
+    __syncwarp();
+    if (c + 1 < chunks) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) s += __shfl_sync(0xffffffffu, v[c], j);
+      for (int k = 0; k < PER; ++k) {
+        const long idx = start + (long)(c + 1) * kStage + k * 32 + lane;
+        v[k] = idx < end ? value(idx) : 0.0;
+      }
+    }
+    if (lane == 0) {
+#pragma unroll 16
+      for (int i = 0; i < kStage; ++i) s += buf[i];
+    }
+    __syncwarp();
   }
-  return s;
+  return __shfl_sync(0xffffffffu, s, 0);
 }
 
-__device__ __noinline__ double pairwise_rec(const double* x, int n) {
-  if (n == 0) return 0.0;
-  if (n == 1) return x[0];
-  const int mid = n / 2;
-  return pairwise_rec(x, mid) + pairwise_rec(x + mid, n - mid);
+// pairwise_sum (P:src/parallel.cpp:81-86) of the leaf partials
+// [lo, lo + n), n <= MAX, as straight-line code: the recursion unrolled at
+// compile time (no stack, no local buffer).  A node of size 1 is its leaf,
+// a node of size 0 is 0.0, children split at n / 2, exactly as the
+// reference recursion.
+template <int MAX>
+__device__ __forceinline__ double pairwise_fixed(const PartView& v, int q, long lo, int n) {
+  if constexpr (MAX <= 1) {
+    return n == 1 ? leaf_part(v, q, lo) : 0.0;
+  } else {
+    if (n <= 1) return n == 1 ? leaf_part(v, q, lo) : 0.0;
+    const int mid = n / 2;
+    return pairwise_fixed<MAX / 2>(v, q, lo, mid) +
+           pairwise_fixed<(MAX + 1) / 2>(v, q, lo + mid, n - mid);
+  }
 }
 
-// pairwise_sum (P:src/parallel.cpp:81-86) of one quantity's leaf partials
-// by one warp.  Lane k walks the top five midpoint splits along the bits of
-// k, sums its depth-5 subtree serially with the same recursion, and the 31
-// internal nodes above are rebuilt with shuffles as left + right.  A node of
-// size 1 passes its single leaf through and a node of size 0 is 0.0, as the
-// reference recursion returns them, so the result is bit-identical.
+// pairwise_sum of one quantity's leaf partials by one warp.  Lane k walks
+// the top five midpoint splits along the bits of k, sums its depth-5
+// subtree with the same recursion (straight-line up to 64 leaves per lane,
+// i.e. 2,048 leaves = 2M genes; the plain recursion beyond), and the 31
+// internal nodes above are rebuilt with shuffles as left + right.  A node
+// of size 1 passes its single leaf through and a node of size 0 is 0.0, as
+// the reference recursion returns them, so the result is bit-identical.
 __device__ double warp_pairwise_leaves(const PartView pv, int q, int n) {
   const int lane = threadIdx.x & 31;
   int lo = 0, cnt = n;
@@ -924,14 +961,8 @@ __device__ double warp_pairwise_leaves(const PartView pv, int q, int n) {
       cnt = mid;
     }
   }
-  double v;
-  if (cnt <= 64) {
-    double buf[64];
-    for (int i = 0; i < cnt; ++i) buf[i] = leaf_part(pv, q, lo + i);
-    v = pairwise_rec(buf, cnt);
-  } else {
-    v = pairwise_leaves(pv, q, lo, cnt);
-  }
+  const double v0 = cnt <= 64 ? pairwise_fixed<64>(pv, q, lo, cnt) : pairwise_leaves(pv, q, lo, cnt);
+  double v = v0;
 #pragma unroll
   for (int d = 4; d >= 0; --d) {
     const int bit = 4 - d;
@@ -947,6 +978,111 @@ __device__ double warp_pairwise_leaves(const PartView pv, int q, int n) {
   return v;
 }
 
+template <bool XI>
+__device__ void hyper_a_body(const SweepParams& p, int slot, long m);
+
+// Leaf sums of partA's quantities for leaf lb of one chain: log gamma
+// (q = 0), 1/gamma (1), beta_l (2 + l); with a xi prior S_l = beta_l/xi_l
+// on xi columns and W_l = 1/xi_l (2 + L + l).  The reference tree's leaves
+// (P:include/countmc/parallel.hpp:67-84): each sum runs serially in gene
+// order.  The block's warps stride over the quantities, each staging
+// through its own kStage buffer; loads bypass L1 (__ldcg) because the
+// gene kernel's other blocks wrote the values.
+template <bool XI>
+__device__ void leaf_a_sums(const SweepParams& p, int slot, long lb, double* stage) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int L = p.L, Q = leaf_q_a(L, p.xi_any), Qs = leaf_qs_a(L, p.xi_any);
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const long start = lb * kLeaf;
+  const long end = min((long)G, start + kLeaf);
+  const long lpr = p.leaves_per_rank;
+  const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
+  double* buf = stage + (size_t)warp * kStage;
+  for (int q = warp; q < Q; q += nwarps) {
+    double s;
+    if (q < 2) {
+      const double* src = (q == 0 ? p.log_gam : p.inv_gam) + so * G;
+      s = warp_serial_sum([&](long i) { return __ldcg(src + i); }, start, end, buf);
+    } else if (q < 2 + L) {
+      const double* src = p.beta + so * L * G + (size_t)(q - 2) * G;
+      if (XI && p.xi_fam[q - 2] != CMC_PRIOR_NORMAL) {  // extension: beta / xi
+        const double* xs = p.xi + so * L * G + (size_t)(q - 2) * G;
+        s = warp_serial_sum([&](long i) { return __ldcg(src + i) / __ldcg(xs + i); }, start,
+                            end, buf);
+      } else {
+        s = warp_serial_sum([&](long i) { return __ldcg(src + i); }, start, end, buf);
+      }
+    } else {  // extension: 1 / xi
+      const double* xs = p.xi + so * L * G + (size_t)(q - 2 - L) * G;
+      s = warp_serial_sum([&](long i) { return 1.0 / __ldcg(xs + i); }, start, end, buf);
+    }
+    if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Qs + q) * lpr + lb] = s;
+  }
+}
+
+// This rank's stall flag of a chain in the gathered partA section (sharded
+// runs): leaf slot 0 of quantity Q.
+__device__ __forceinline__ void write_stall_flag(const SweepParams& p, int slot, bool st) {
+  const long lpr = p.leaves_per_rank;
+  const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
+  const int Q = leaf_q_a(p.L, p.xi_any), Qs = leaf_qs_a(p.L, p.xi_any);
+  p.partA[((rank * p.C + (slot - p.slot_base)) * Qs + Q) * lpr] = st ? 1.0 : 0.0;
+}
+
+// End of the gene kernel (no xi prior): the leaf reductions fused into the
+// update kernel.  The last of a leaf's (up to) 8 blocks to finish sums the
+// leaf for its chain (hyper_a_kernel then reduces the leaves and draws nu,
+// tau, theta).  Sharded, the last leaf of the chain also writes this
+// rank's stall flag for the all-gather.  Every block of the grid takes
+// part, also when the chain stalled (the body then did nothing), so the
+// per-leaf counters always return to 0.
+template <bool XI>
+__device__ void gene_leaf_epilogue(const SweepParams& p, int slot, long m, double* stage) {
+  __shared__ int s_role;
+  const int tid = threadIdx.x;
+  Hyper* hp = p.hyper + slot;
+  const long lb = blockIdx.x / kBlocksPerLeaf;
+  __threadfence();  // this thread's gamma/beta stores before the count
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned nb = min((unsigned)kBlocksPerLeaf, gridDim.x - (unsigned)lb * kBlocksPerLeaf);
+    unsigned* cnt = p.leaf_cnt + (size_t)slot * p.n_leaves_local + lb;
+    const bool last = atomicAdd(cnt, 1u) == nb - 1;
+    if (last) *cnt = 0;
+    s_role = last ? 1 : 0;
+  }
+  __syncthreads();
+  if (!s_role) return;
+  __threadfence();
+  leaf_a_sums<XI>(p, slot, lb, stage);
+  if (p.fuse_tail) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const bool last = atomicAdd(&hp->doneA, 1u) == (unsigned)p.n_leaves_local - 1;
+    if (last) {
+      hp->doneA = 0;
+      __threadfence();
+      write_stall_flag(p, slot, tail_stalled(hp, m));
+    }
+  }
+}
+
+template <int JR, bool XI>
+__global__ void __launch_bounds__(kGeneThreads, CMC_GENE_MIN_BLOCKS)
+    gene_sweep_kernel(const SweepParams p, const long m_off) {
+  extern __shared__ double smem[];
+  __shared__ double exp_tab[32];
+  exp_table_init(exp_tab);
+  __syncthreads();
+  gene_sweep_body<JR, XI>(p, m_off, smem, ExpTab(exp_tab));
+  // the lp buffer (at least 4 x 128 doubles, gene_sweep_smem_bytes) is free
+  // now: it stages the leaf sums
+  if constexpr (!XI) {
+    if (p.fuse_leaf_a) gene_leaf_epilogue<XI>(p, p.slot_base + blockIdx.y, *p.d_m + m_off, smem);
+  }
+}
+
 // Steps 3, 4 and 6: nu, tau and theta from the gathered leaf sums.  Called
 // by a whole block of 32*(2+L) threads (warp q reduces quantity q).
 template <bool XI>
@@ -955,11 +1091,11 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
   Hyper* hp = p.hyper + slot;
   const int tid = threadIdx.x, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint64_t chain = (uint64_t)(p.chain_base + (slot - p.slot_base));
-  const int L = p.L, Q = leaf_q_a(L, p.xi_any);
+  const int L = p.L, Q = leaf_q_a(L, p.xi_any), Qs = leaf_qs_a(L, p.xi_any);
   const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
   const double Gd = (double)p.G_total;
   for (int q = warp; q < Q; q += nwarps) {  // Q may exceed the block's warps
-    const double r = warp_pairwise_leaves(part_view(p.partA, p, slot, Q), q, p.n_leaves_total);
+    const double r = warp_pairwise_leaves(part_view(p.partA, p, slot, Qs), q, p.n_leaves_total);
     if ((tid & 31) == 0) red[q] = r;
   }
   __syncthreads();
@@ -1114,102 +1250,91 @@ __device__ __forceinline__ bool last_block(unsigned int* counter, unsigned total
   return is_last;
 }
 
-// Leaf sums of log gamma (q=0), 1/gamma (q=1), beta_l (q=2+l); one warp
-// per quantity, one block per local leaf.
-// Tail kernels run at most kTailWarps warps per block (registers for 512
-// threads are guaranteed); warps loop over the 2 + L (+ L) quantities.
+// Leaf sums of partA's quantities (leaf_a_sums) as their own kernel, one
+// block per local leaf and chain: used with a xi prior, whose S_l and W_l
+// need the xi kernel's draws (without one the gene kernel sums its leaves,
+// gene_leaf_epilogue).  One GPU: the last block runs steps 3, 4 and 6.
+// Sharded: block 0 writes this rank's stall flag for the all-gather.  Tail
+// kernels run at most kTailWarps warps per block (registers for 512
+// threads are guaranteed); warps loop over the quantities.
 template <bool XI>
 __global__ void __launch_bounds__(32 * kTailWarps) leaf_a_kernel(const SweepParams p,
                                                                  const long m_off) {
+  __shared__ double stage[kTailWarps][kStage];
   WarpTrace wt(p, 3, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
-  if (stalled_chain(hp)) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int L = p.L, Q = leaf_q_a(L, p.xi_any);
-  const size_t G = (size_t)p.G, so = (size_t)slot;
-  const long lb = blockIdx.x;
-  const long start = lb * kLeaf;
-  const long end = min((long)G, start + kLeaf);
-  const long lpr = p.leaves_per_rank;
-  const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
-  if constexpr (!XI) {
-    for (int q = warp; q < Q; q += nwarps) {
-      const double* src = q == 0   ? p.log_gam + so * G
-                          : q == 1 ? p.inv_gam + so * G
-                                   : p.beta + so * L * G + (size_t)(q - 2) * G;
-      const double s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
-      if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Q + q) * lpr + lb] = s;
-    }
-  } else {
-    // xi engine: quantities [log gamma, 1/gamma, S_l, W_l] (sweep.h), looped
-    // when Q exceeds the 32 warps of a block
-    for (int q = warp; q < Q; q += nwarps) {
-      double s;
-      if (q < 2) {
-        const double* src = q == 0 ? p.log_gam + so * G : p.inv_gam + so * G;
-        s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
-      } else if (q < 2 + L) {
-        const double* src = p.beta + so * L * G + (size_t)(q - 2) * G;
-        if (p.xi_fam[q - 2] != CMC_PRIOR_NORMAL) {
-          const double* xs = p.xi + so * L * G + (size_t)(q - 2) * G;
-          s = warp_leaf_sum([&](long i) { return src[i] / xs[i]; }, start, end);
-        } else {
-          s = warp_leaf_sum([&](long i) { return src[i]; }, start, end);
-        }
-      } else {
-        const double* xs = p.xi + so * L * G + (size_t)(q - 2 - L) * G;
-        s = warp_leaf_sum([&](long i) { return 1.0 / xs[i]; }, start, end);
-      }
-      if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Q + q) * lpr + lb] = s;
-    }
-  }
+  const long m = *p.d_m + m_off;
+  const bool st = tail_stalled(hp, m);
+  if (!p.fuse_tail && blockIdx.x == 0 && threadIdx.x == 0) write_stall_flag(p, slot, st);
+  if (st) return;
+  leaf_a_sums<XI>(p, slot, blockIdx.x, &stage[0][0]);
   if (!p.fuse_tail) return;
   if (!last_block(&hp->doneA, (unsigned)p.n_leaves_local)) return;
-  hyper_a_body<XI>(p, slot, *p.d_m + m_off);
+  hyper_a_body<XI>(p, slot, m);
 }
 
+// Steps 3, 4 and 6 from the leaf sums (one block per chain): after the
+// gene kernel's fused leaf sums on one GPU, after the all-gather when
+// sharded.  Sharded, every rank's stall flag is checked first: if a rank's
+// chain stalled, every rank stops the chain here (identically, from the
+// same gathered flags) and sync reports the stalling rank's record.
 template <bool XI>
 __global__ void __launch_bounds__(32 * kTailWarps) hyper_a_kernel(const SweepParams p,
                                                                   const long m_off) {
   const int slot = p.slot_base + blockIdx.x;
-  if (stalled_chain(p.hyper + slot)) return;
-  hyper_a_body<XI>(p, slot, *p.d_m + m_off);
+  WarpTrace wt(p, 5, slot);
+  Hyper* hp = p.hyper + slot;
+  const long m = *p.d_m + m_off;
+  if (tail_stalled(hp, m)) return;
+  const int Q = leaf_q_a(p.L, p.xi_any), Qs = leaf_qs_a(p.L, p.xi_any);
+  const long lpr = p.leaves_per_rank, c = slot - p.slot_base;
+  for (int r = 0; r < p.world && !p.fuse_tail; ++r)
+    if (__ldcg(p.partA + ((r * p.C + c) * Qs + Q) * lpr) != 0.0) {
+      if (threadIdx.x == 0) hp->peer_stall = 1u;
+      return;
+    }
+  hyper_a_body<XI>(p, slot, m);
 }
 
-// Leaf sums of (beta_l - theta_l)^2 with theta of this iteration.
+// Leaf sums of (beta_l - theta_l)^2 with theta of this iteration (one warp
+// per column, staged like leaf_a_sums); one GPU: the last block draws sigma
+// (step 7) and updates the hyper monitors.
 template <bool XI>
 __global__ void __launch_bounds__(32 * kTailWarps) leaf_b_kernel(const SweepParams p,
                                                                  const long m_off) {
+  __shared__ double stage[kTailWarps][kStage];
   WarpTrace wt(p, 4, p.slot_base + blockIdx.y);
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
-  if (stalled_chain(hp)) return;
+  const long m = *p.d_m + m_off;
+  if (tail_stalled(hp, m)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.L;
   const size_t G = (size_t)p.G, so = (size_t)slot;
   const long lb = blockIdx.x;
   const long start = lb * kLeaf;
   const long end = min((long)G, start + kLeaf);
+  double* buf = &stage[warp][0];
   for (int q = warp; q < L; q += blockDim.x >> 5) {
     const double th = hp->theta[q];
     const double* src = p.beta + so * L * G + (size_t)q * G;
     double s;
     if (XI && p.xi_fam[q] != CMC_PRIOR_NORMAL) {  // extension: /xi
       const double* xs = p.xi + so * L * G + (size_t)q * G;
-      s = warp_leaf_sum(
+      s = warp_serial_sum(
           [&](long i) {
             const double dl = src[i] - th;
             return dl * dl / xs[i];
           },
-          start, end);
+          start, end, buf);
     } else {
-      s = warp_leaf_sum(
+      s = warp_serial_sum(
           [&](long i) {
             const double dl = src[i] - th;
             return dl * dl;
           },
-          start, end);
+          start, end, buf);
     }
     if (lane == 0) {
       const long lpr = p.leaves_per_rank;
@@ -1219,14 +1344,15 @@ __global__ void __launch_bounds__(32 * kTailWarps) leaf_b_kernel(const SweepPara
   }
   if (!p.fuse_tail) return;
   if (!last_block(&hp->doneB, (unsigned)p.n_leaves_local)) return;
-  hyper_b_body(p, slot, *p.d_m + m_off);
+  hyper_b_body(p, slot, m);
 }
 
 __global__ void __launch_bounds__(32 * kTailWarps) hyper_b_kernel(const SweepParams p,
                                                                   const long m_off) {
   const int slot = p.slot_base + blockIdx.x;
-  if (stalled_chain(p.hyper + slot)) return;
-  hyper_b_body(p, slot, *p.d_m + m_off);
+  const long m = *p.d_m + m_off;
+  if (tail_stalled(p.hyper + slot, m)) return;
+  hyper_b_body(p, slot, m);
 }
 
 // Per-gene contrasts that read hyperparameters of the same iteration: run
@@ -1234,10 +1360,10 @@ __global__ void __launch_bounds__(32 * kTailWarps) hyper_b_kernel(const SweepPar
 __global__ void gene_contrast_kernel(const SweepParams p, const long m_off) {
   const int slot = p.slot_base + blockIdx.y;
   const Hyper* hp = p.hyper + slot;
-  if (stalled_chain(hp)) return;
+  const long m = *p.d_m + m_off;
+  if (tail_stalled(hp, m)) return;
   const long gl = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gl >= p.G) return;
-  const long m = *p.d_m + m_off;
   if (!(p.monitor_enabled && m > p.burnin)) return;
   const double mc = (double)(m - p.burnin);
   const size_t G = (size_t)p.G, so = (size_t)slot;
@@ -1285,7 +1411,11 @@ cudaError_t launch_prio(K kernel, dim3 grid, dim3 block, size_t smem,
 }
 
 int gene_sweep_smem_bytes(int N, int Jmax) {
-  return (int)(sizeof(double) * (size_t)(N + 2 * Jmax) * kGeneThreads);
+  // lp [N][B] and the group sums [2 Jmax][B]; at least kGeneThreads / 32
+  // staging rows of kStage for the fused leaf sums
+  const int rows = N + 2 * Jmax;
+  const int stage_rows = (kGeneThreads / 32) * kStage / kGeneThreads;
+  return (int)(sizeof(double) * (size_t)(rows > stage_rows ? rows : stage_rows) * kGeneThreads);
 }
 
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
@@ -1295,16 +1425,41 @@ cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
 }
 
 template <int JR, bool XI>
+static cudaError_t raise_smem(int dyn, int optin, int* total) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, gene_sweep_kernel<JR, XI>);
+  if (e != cudaSuccess) return e;
+  *total = (int)fa.sharedSizeBytes + dyn;
+  if (*total > optin) return cudaSuccess;  // the caller reports CMC_ERR_CONFIG
+  if (dyn > fa.maxDynamicSharedSizeBytes)
+    e = cudaFuncSetAttribute(gene_sweep_kernel<JR, XI>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  return e;
+}
+
+// The attribute is per device: every engine sets it on its own device when
+// it allocates (ensure_device), for the one gene kernel variant it launches,
+// under one process-wide lock so engines of one device (loopback ranks)
+// only ever raise it.  *total = static + dynamic bytes per block.
+cudaError_t configure_gene_kernels(int N, int Jmax, int xi_any, int* total) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) !=
+      cudaSuccess)
+    return e;
+  const int jr = Jmax <= 2;
+  const int dyn = gene_sweep_smem_bytes(N, jr ? 0 : Jmax);
+  if (jr) return xi_any ? raise_smem<2, true>(dyn, optin, total) : raise_smem<2, false>(dyn, optin, total);
+  return xi_any ? raise_smem<0, true>(dyn, optin, total) : raise_smem<0, false>(dyn, optin, total);
+}
+
+template <int JR, bool XI>
 static cudaError_t launch_gene_sweep_t(const SweepParams& p, int chains, long m_off,
                                        cudaStream_t s) {
   const int smem = gene_sweep_smem_bytes(p.N, JR > 0 ? 0 : p.Jmax);
-  static int configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(
-        gene_sweep_kernel<JR, XI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
   dim3 grid((unsigned)((p.G + kGeneThreads - 1) / kGeneThreads), (unsigned)chains);
   return launch_prio(gene_sweep_kernel<JR, XI>, grid, dim3(kGeneThreads), smem, s, p.prio_gene, p,
                      m_off);

@@ -31,7 +31,7 @@ slot = ((r[:, 0] >> 48) & 0xff).astype(int)
 t0 = r[:, 1].min()
 st = (r[:, 1] - t0) / 1e3
 en = (r[:, 2] - t0) / 1e3
-names = {1: "eps", 2: "gene", 3: "leaf_a", 4: "leaf_b"}
+names = {1: "eps", 2: "gene", 3: "leaf_a", 4: "leaf_b", 5: "hyper_a"}
 lanes = 2 if C >= 2 else 1
 lane = slot * lanes // C
 rows = []

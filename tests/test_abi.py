@@ -132,7 +132,7 @@ def test_sample_count_beyond_gene_kernel_shared_memory():
     from paper_1606_06659_b200 import builtin_design
     X = builtin_design("heterosis16x5", 240)
     counts = np.ones((8, 240), np.int64)
-    with pytest.raises(ConfigError, match="at most 227 samples"):
+    with pytest.raises(ConfigError, match="at most 226 samples"):
         GibbsEngine(CountMatrix(counts), ModelSpec(X, np.zeros(240)),
                     RunConfig(chains=1, burnin=10, iterations=10))
     X = builtin_design("heterosis16x5", 224)   # fits
