@@ -152,9 +152,11 @@ typedef struct cmc_output_view {
   long* sample_iters;
   uint64_t* clamp_events;
   double* final_state;
-  double* step_seconds; /* [7]; the fused sweep reports its device time in
-                           slot 0 (steps 1,2,5 are one kernel) and the hyper
-                           tail in slot 2 */
+  double* step_seconds; /* [7], the reference StepTimings order (epsilon,
+                           gamma, nu, tau, beta, theta, sigma): per-step
+                           device seconds after a run in the per-step timing
+                           mode (cmc_engine_set_step_timing), else the fused
+                           sweep's device time in slot 0 */
 } cmc_output_view;
 
 typedef struct cmc_engine cmc_engine;
@@ -214,6 +216,12 @@ int cmc_engine_begin(cmc_engine* engine, cmc_error* err);
 int cmc_engine_sweeps(cmc_engine* engine, long m_begin, long m_end,
                       cmc_error* err);
 int cmc_engine_sync(cmc_engine* engine, cmc_error* err);
+/* Per-step timing mode (debug; reference StepTimings, engine.hpp:86-88 and
+ * engine.cpp:173-176): while on, sweeps() launches each step on its own
+ * (the gene kernel split into its step-2 and step-5 launches) with CUDA
+ * events between them, and get_output()/write_results() report seconds per
+ * step; results are bit-identical, the sweep is slower.  Single GPU. */
+int cmc_engine_set_step_timing(cmc_engine* engine, int on);
 /* Capture (and cache) the CUDA graphs a sweeps() call of `sweeps` sweeps
  * replays, without running them: moves the one-time capture cost out of a
  * timed region.  After begin(); no reference counterpart. */

@@ -38,7 +38,7 @@ EXPORTS = [
     "cmc_engine_saved_genes", "cmc_engine_config", "cmc_engine_initial_state",
     "cmc_engine_set_state", "cmc_engine_get_state", "cmc_engine_iterate",
     "cmc_engine_run", "cmc_engine_begin", "cmc_engine_sweeps", "cmc_engine_sync",
-    "cmc_engine_prepare",
+    "cmc_engine_prepare", "cmc_engine_set_step_timing",
     "cmc_engine_stream", "cmc_engine_launches_per_sweep", "cmc_engine_profile",
     "cmc_engine_profile_phases",
     "cmc_engine_trace", "cmc_engine_diagnostics", "cmc_engine_write_results",
@@ -224,6 +224,7 @@ def load_library(path: str = LIB_PATH):
     lib.cmc_engine_sweeps.argtypes = [c_void_p, c_long, c_long, E]
     lib.cmc_engine_sync.argtypes = [c_void_p, E]
     lib.cmc_engine_prepare.argtypes = [c_void_p, c_long, E]
+    lib.cmc_engine_set_step_timing.argtypes = [c_void_p, c_int]
     lib.cmc_engine_stream.argtypes = [c_void_p]
     lib.cmc_engine_stream.restype = c_void_p
     lib.cmc_engine_launches_per_sweep.argtypes = [c_void_p]

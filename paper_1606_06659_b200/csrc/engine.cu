@@ -299,6 +299,12 @@ struct cmc_engine {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timing_pending = false;
   double sweep_seconds = 0.0;
+  // per-step timing mode (cmc_engine_set_step_timing): sweeps launch one
+  // step at a time with CUDA events between the steps; per-chain seconds of
+  // the reference's 7 steps (StepTimings, P:include/countmc/engine.hpp:86-88)
+  bool step_timing = false, step_timed = false;
+  std::vector<double> step_sec;           // [C][7]
+  DevBuf<unsigned long long> step_cyc;    // [slots][4]
   bool begun = false;
   long n_cols = 0, n_rows = 0;
 };
@@ -437,7 +443,9 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   const long n_leaves_local = (G + kLeaf - 1) / kLeaf;
   CUDA_TRY(e->leaf_cnt.alloc((size_t)Cs * n_leaves_local));
   CUDA_TRY(cudaMemset(e->leaf_cnt.p, 0, sizeof(unsigned int) * e->leaf_cnt.n));
-  if (e->world > 1) CUDA_TRY(e->stall_x.alloc((size_t)e->world * Cs * 4));
+  CUDA_TRY(e->step_cyc.alloc((size_t)Cs * 4));
+  CUDA_TRY(cudaMemset(e->step_cyc.p, 0, sizeof(unsigned long long) * e->step_cyc.n));
+  if (e->split_tail) CUDA_TRY(e->stall_x.alloc((size_t)e->world * Cs * 4));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_coll, cudaEventDisableTiming));
   CUDA_TRY(e->partB.alloc((size_t)e->world * Cs * L * lpr));
   CUDA_TRY(e->dctab.alloc(1));
@@ -883,11 +891,11 @@ int check_stall(cmc_engine* e, long slot_lo, long slot_hi, cmc_error* err) {
   std::vector<StallRec> recs((size_t)n);
   for (long c = slot_lo; c < slot_hi; ++c) CUDA_TRY(local_stall(e, c, &recs[(size_t)(c - slot_lo)]));
   std::vector<StallRec> all = recs;
-  if (e->world > 1) {
+  if (e->split_tail) {  // sharded (a 1-rank clique included)
     const int rc = exchange_stalls(e, slot_lo, slot_hi, recs, all, err);
     if (rc) return rc;
   }
-  const int W = e->world > 1 ? e->world : 1;
+  const int W = e->split_tail ? e->world : 1;
   for (long i = 0; i < n; ++i) {
     const StallRec* best = nullptr;
     for (int r = 0; r < W; ++r) {
@@ -1374,6 +1382,7 @@ int cmc_engine_destroy(cmc_engine* e) {
     e->saved_slot.free_();
     e->hyper.free_();
     e->leaf_cnt.free_();
+    e->step_cyc.free_();
     e->stall_x.free_();
     if (e->ev_coll) cudaEventDestroy(e->ev_coll);
     e->dctab.free_();
@@ -1505,7 +1514,7 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
   if (clamps) *clamps += hp.clamps - before;
   if ((rc = set_device_m(e, run_m, err))) return rc;
   // sharded: every rank takes part in the record exchange, stalled or not
-  if (e->world > 1 || hp.err_key != kNoError || hp.err_key_eps != kNoError)
+  if (e->split_tail || hp.err_key != kNoError || hp.err_key_eps != kNoError)
     return check_stall(e, slot, slot + 1, err);
   return CMC_OK;
 }
@@ -1535,7 +1544,95 @@ int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaMemcpy(e->d_m.p, &one, sizeof(long), cudaMemcpyHostToDevice));
   e->host_m = 1;
   e->sweep_seconds = 0.0;
+  e->step_timed = false;
+  e->step_sec.assign((size_t)e->C * 7, 0.0);
+  CUDA_TRY(cudaMemset(e->step_cyc.p, 0, sizeof(unsigned long long) * e->step_cyc.n));
   e->begun = true;
+  return CMC_OK;
+}
+
+// Per-step timing mode: each sweep's steps launched one at a time for all
+// chains on the engine stream, CUDA events between them: eps (step 1), the
+// gene kernel split into its step-2 and step-5 launches (the latter with
+// the fused leaf sums, and the xi kernel with a xi prior), hyper_a (steps
+// 3, 4, 6; leaf_a with a xi prior), leaf_b (step 7).  The nu / tau / theta
+// draws inside hyper_a are told apart by the kernel's clock64 stamps; the
+// rest of that kernel (the leaf reductions, launch) is charged to nu.  A
+// launch covers all chains, so each chain is charged 1/C of it.  Results
+// are bit-identical to the fused schedule (same kernels, same order of
+// dependent steps).  Single GPU only.
+int step_timed_sweeps(cmc_engine* e, const SweepParams& p_in, long total, cmc_error* err) {
+  if (e->split_tail || e->loop) {
+    set_err(err, CMC_ERR_ARG, "per-step timing is single-GPU only");
+    return CMC_ERR_ARG;
+  }
+  SweepParams p = p_in;
+  p.C = (int)e->C;
+  p.step_cycles = e->step_cyc.p;
+  cudaStream_t s = e->stream;
+  CUDA_TRY(cudaStreamWaitEvent(s, e->ev_tail, 0));
+  for (int k = 1; k < e->n_lanes; ++k) CUDA_TRY(cudaStreamWaitEvent(s, e->lanes[k].ev_tail, 0));
+  constexpr int P = 6;
+  std::vector<cudaEvent_t> ev((size_t)(P + 1) * total);
+  for (auto& x : ev) CUDA_TRY(cudaEventCreate(&x));
+  std::vector<unsigned long long> cyc0(e->step_cyc.n);
+  CUDA_TRY(cudaMemcpy(cyc0.data(), e->step_cyc.p, sizeof(unsigned long long) * cyc0.size(),
+                      cudaMemcpyDeviceToHost));
+  for (long off = 0; off < total; ++off) {
+    cudaEvent_t* E = ev.data() + (P + 1) * off;
+    CUDA_TRY(cudaEventRecord(E[0], s));
+    CUDA_TRY(launch_eps_sweep(p, e->C, off, s));
+    CUDA_TRY(cudaEventRecord(E[1], s));
+    CUDA_TRY(launch_gene_sweep(p, e->C, off, s, 1));
+    CUDA_TRY(cudaEventRecord(E[2], s));
+    CUDA_TRY(launch_gene_sweep(p, e->C, off, s, 2));
+    if (e->xi_any) CUDA_TRY(launch_xi_sweep(p, e->C, off, s));
+    CUDA_TRY(cudaEventRecord(E[3], s));
+    CUDA_TRY(p.fuse_leaf_a ? launch_hyper_a(p, e->C, off, s) : launch_leaf_a(p, e->C, off, s));
+    CUDA_TRY(cudaEventRecord(E[4], s));
+    CUDA_TRY(launch_leaf_b(p, e->C, off, s));
+    CUDA_TRY(cudaEventRecord(E[5], s));
+    if (p.monitor_enabled && e->has_ctab && e->ctab.gene_needs_hyper)
+      CUDA_TRY(launch_gene_contrast(p, e->C, off, s));
+    CUDA_TRY(cudaEventRecord(E[6], s));
+  }
+  CUDA_TRY(launch_advance(e->d_m.p, total, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  double ms[P] = {0, 0, 0, 0, 0, 0};
+  for (long off = 0; off < total; ++off)
+    for (int k = 0; k < P; ++k) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, ev[(P + 1) * off + k], ev[(P + 1) * off + k + 1]));
+      ms[k] += t;
+    }
+  for (auto& x : ev) cudaEventDestroy(x);
+  std::vector<unsigned long long> cyc1(e->step_cyc.n);
+  CUDA_TRY(cudaMemcpy(cyc1.data(), e->step_cyc.p, sizeof(unsigned long long) * cyc1.size(),
+                      cudaMemcpyDeviceToHost));
+  int khz = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, e->device));
+  const double sec_per_cycle = khz > 0 ? 1.0 / (khz * 1e3) : 0.0;
+  const double C = (double)e->C;
+  double drawn = 0.0;  // seconds of the tau and theta draws, all chains
+  std::vector<double> d((size_t)e->C * 3);
+  for (long c = 0; c < e->C; ++c)
+    for (int k = 0; k < 3; ++k) {
+      d[(size_t)c * 3 + k] = (double)(cyc1[(size_t)c * 4 + k] - cyc0[(size_t)c * 4 + k]) * sec_per_cycle;
+      if (k) drawn += d[(size_t)c * 3 + k];
+    }
+  const double hyper_rest = std::max(0.0, ms[3] * 1e-3 - drawn / C);
+  for (long c = 0; c < e->C; ++c) {
+    double* st = &e->step_sec[(size_t)c * 7];
+    st[0] += ms[0] * 1e-3 / C;                                // epsilon
+    st[1] += ms[1] * 1e-3 / C;                                // gamma
+    st[2] += hyper_rest / C;                                  // nu (+ the reductions)
+    st[3] += d[(size_t)c * 3 + 1];                            // tau
+    st[4] += ms[2] * 1e-3 / C;                                // beta (+ leaf sums, xi)
+    st[5] += d[(size_t)c * 3 + 2];                            // theta
+    st[6] += (ms[4] + ms[5]) * 1e-3 / C;                      // sigma (+ monitors)
+  }
+  e->sweep_seconds += (ms[0] + ms[1] + ms[2] + ms[3] + ms[4] + ms[5]) * 1e-3;
+  e->step_timed = true;
   return CMC_OK;
 }
 
@@ -1559,6 +1656,11 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
 #ifndef CMC_GRAPH_CHUNK
 #define CMC_GRAPH_CHUNK 50  // sweeps per CUDA graph (A/B: 25 0.3551 ms, 50 0.3531, 100 0.3527)
 #endif
+  if (e->step_timing) {
+    const int rc = step_timed_sweeps(e, p, total, err);
+    if (rc == CMC_OK) e->host_m = m_end;
+    return rc;
+  }
   CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
   if (e->loop) {
     // loopback group: eager launches (another engine's events cannot enter
@@ -1590,6 +1692,12 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
   CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
   e->timing_pending = true;
   e->host_m = m_end;
+  return CMC_OK;
+}
+
+int cmc_engine_set_step_timing(cmc_engine* e, int on) {
+  if (!e) return CMC_ERR_ARG;
+  e->step_timing = on != 0;
   return CMC_OK;
 }
 
@@ -1915,9 +2023,13 @@ int cmc_engine_write_results(cmc_engine* e, const char* outdir, const char* cons
   std::vector<Hyper> hp((size_t)C);
   CUDA_TRY(cudaMemcpy(hp.data(), e->hyper.p, sizeof(Hyper) * C, cudaMemcpyDeviceToHost));
   for (long c = 0; c < C; ++c) {
-    // the device sweep is fused: its time is reported under the first step
+    // per-step timing mode: the 7 steps; otherwise the fused device sweep
+    // under the first step
     std::vector<double> st(7, 0.0);
-    st[0] = e->sweep_seconds;
+    if (e->step_timed)
+      st.assign(e->step_sec.begin() + c * 7, e->step_sec.begin() + c * 7 + 7);
+    else
+      st[0] = e->sweep_seconds;
     in.step_seconds.push_back(st);
     in.clamp_events.push_back(hp[(size_t)c].clamps);
   }
@@ -2033,8 +2145,11 @@ int cmc_engine_get_output(cmc_engine* e, long chain, const cmc_output_view* o,
     if ((rc = download_state(e, chain, o->final_state, nullptr, nullptr, err))) return rc;
   }
   if (o->step_seconds) {
-    for (int k = 0; k < 7; ++k) o->step_seconds[k] = 0.0;
-    o->step_seconds[0] = e->sweep_seconds;
+    // per-step timing mode: the 7 steps; otherwise the fused device sweep
+    // under the first step
+    for (int k = 0; k < 7; ++k)
+      o->step_seconds[k] = e->step_timed ? e->step_sec[(size_t)chain * 7 + k] : 0.0;
+    if (!e->step_timed) o->step_seconds[0] = e->sweep_seconds;
   }
   return CMC_OK;
 }

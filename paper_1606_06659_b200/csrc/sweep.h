@@ -137,6 +137,9 @@ struct SweepParams {
   // optional block timeline (debug/profiling): per record {kernel<<56 |
   // slot<<48 | smid<<32 | blockIdx.x, t_start_ns, t_end_ns}
   unsigned long long* trace;
+  // per-step timing mode: [slots][4] SM clock cycles of the nu, tau and
+  // theta draws inside hyper_a (accumulated; null otherwise)
+  unsigned long long* step_cycles;
   unsigned int* trace_n;
   unsigned int trace_cap;
   // launch priorities (host side): the tail and gene kernels are on the
@@ -164,8 +167,10 @@ constexpr int kStage = 128;  // values per warp per staging round of the serial 
 // Launch wrappers (sweep_kernels.cu).  `chains` = grid.y.
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
                              cudaStream_t s);
+// phase: 3 the whole gene kernel (steps 2 and 5), 1 step 2 only, 2 step 5
+// only (the per-step timing mode)
 cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
-                              cudaStream_t s);
+                              cudaStream_t s, int phase = 3);
 cudaError_t launch_xi_sweep(const SweepParams& p, int chains, long m_off,
                             cudaStream_t s);
 cudaError_t launch_leaf_a(const SweepParams& p, int chains, long m_off,

@@ -616,7 +616,9 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 // (BetaFR); JR = 0: any design, group sums in shared memory (BetaF).
 // XI: some column has a xi prior (extension); the reference model (all
 // normal) is compiled without the xi step.
-template <int JR, bool XI>
+// PH: the steps this launch runs, bit 0 step 2 (gamma), bit 1 step 5
+// (beta); the sweep runs both (3), the per-step timing mode one at a time.
+template <int JR, bool XI, int PH>
 __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long m_off,
                                                 double* smem, const ExpTab etab) {
   WarpTrace wt(p, 2, p.slot_base + blockIdx.y);
@@ -651,22 +653,25 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
   // lp_n = (h_n + eps_n) + xb_n with the new eps and the previous beta,
   // and ss = sum_n eps_n^2 in n order (P:src/engine.cpp:275-283,
   // P:src/model.cpp:76-82)
-  for (int n = 0; n < N; ++n) xs[n * kGeneThreads + tid] = 0.0;
-  for (int l = 0; l < L; ++l) {
-    const double b = alive ? beta[(size_t)l * G + gl] : 0.0;
-    for (int n = 0; n < N; ++n)
-      xs[n * kGeneThreads + tid] += __ldg(p.X + n * L + l) * b;
+  constexpr bool GAM = (PH & 1) != 0, BET = (PH & 2) != 0;
+  if constexpr (BET) {
+    for (int n = 0; n < N; ++n) xs[n * kGeneThreads + tid] = 0.0;
+    for (int l = 0; l < L; ++l) {
+      const double b = alive ? beta[(size_t)l * G + gl] : 0.0;
+      for (int n = 0; n < N; ++n)
+        xs[n * kGeneThreads + tid] += __ldg(p.X + n * L + l) * b;
+    }
   }
   const double gam_old = alive ? p.gam[so * G + gl] : 1.0;
   double ss = 0.0;
   for (int n = 0; n < N; ++n) {
     const double e = alive ? eps[(size_t)n * G + gl] : 0.0;
-    ss += e * e;
-    xs[n * kGeneThreads + tid] = __ldg(p.h + n) + e + xs[n * kGeneThreads + tid];
+    if constexpr (GAM) ss += e * e;
+    if constexpr (BET) xs[n * kGeneThreads + tid] = __ldg(p.h + n) + e + xs[n * kGeneThreads + tid];
   }
 
   // Step 2: gamma_g, P:src/engine.cpp:204-226 (nu, tau of iteration m-1)
-  {
+  if constexpr (GAM) {
     double gnew = gam_old, w0 = 0.0, w = 0.0, wa = 0.0;
     bool st = false;
     __syncwarp();
@@ -704,124 +709,126 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
     }
   }
 
-  // Step 5: beta_g1..beta_gL in column order, P:src/engine.cpp:269-334
-  for (int l = 0; l < L; ++l) {
-    const size_t i = (size_t)l * G + gl;
-    const int jb = __ldg(p.grp_off + l), je = __ldg(p.grp_off + l + 1);
-    const bool xcol = XI && p.xi_fam[l] != CMC_PRIOR_NORMAL;  // warp-uniform
-    double bold = 0.0, bnew = 0.0, w0 = 0.0, w = 0.0, wa = 0.0;
-    bool st = false;
-    __syncwarp();
-    if (alive) {
-      bold = beta[i];
-      // S_j = sum over the group's samples, in order, of
-      // clamped_exp(lp_n - v_j * bold) (P:src/engine.cpp:295-300)
-      auto group_sum = [&](int j) {
-        const double v = __ldg(p.grp_val + j);
-        const double vb = v * bold;
-        const int q0 = __ldg(p.grp_moff + j), q1 = __ldg(p.grp_moff + j + 1);
-        double s = 0.0;
-        for (int q = q0; q < q1; ++q) {
-          const int n = __ldg(p.grp_mem + q);
-          double t = xs[n * kGeneThreads + tid] - vb;
-          if (t > kExpClamp) {
-            ++clamps;
-            t = kExpClamp;
+  if constexpr (BET) {
+    // Step 5: beta_g1..beta_gL in column order, P:src/engine.cpp:269-334
+    for (int l = 0; l < L; ++l) {
+      const size_t i = (size_t)l * G + gl;
+      const int jb = __ldg(p.grp_off + l), je = __ldg(p.grp_off + l + 1);
+      const bool xcol = XI && p.xi_fam[l] != CMC_PRIOR_NORMAL;  // warp-uniform
+      double bold = 0.0, bnew = 0.0, w0 = 0.0, w = 0.0, wa = 0.0;
+      bool st = false;
+      __syncwarp();
+      if (alive) {
+        bold = beta[i];
+        // S_j = sum over the group's samples, in order, of
+        // clamped_exp(lp_n - v_j * bold) (P:src/engine.cpp:295-300)
+        auto group_sum = [&](int j) {
+          const double v = __ldg(p.grp_val + j);
+          const double vb = v * bold;
+          const int q0 = __ldg(p.grp_moff + j), q1 = __ldg(p.grp_moff + j + 1);
+          double s = 0.0;
+          for (int q = q0; q < q1; ++q) {
+            const int n = __ldg(p.grp_mem + q);
+            double t = xs[n * kGeneThreads + tid] - vb;
+            if (t > kExpClamp) {
+              ++clamps;
+              t = kExpClamp;
+            }
+            s += fast_exp(t, etab);
           }
-          s += fast_exp(t, etab);
-        }
-        return s;
-      };
-      const double sig = hp->sigma[l];
-      const double sig2 = sig * sig;
-      // prior variance sigma_l^2 (normal) or sigma_l^2 xi_gl (xi column)
-      const double inv2v = xcol ? 1.0 / (2.0 * (sig2 * p.xi[so * L * G + i]))
-                                : 1.0 / (2.0 * sig2);
-      w0 = beta_w[i];
-      w = w0;
-      wa = tuning ? beta_wa[i] : 0.0;
-      Stream rng;
-      rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l));
-      if constexpr (JR > 0) {
-        BetaFR<JR> f;
-        f.a = __ldg(p.A + i);
-        f.theta = hp->theta[l];
-        f.inv_two_sig2 = inv2v;
-        f.e700 = p.exp_clamp;
-        f.tab = etab;
-        f.J = je - jb;
-        f.clamps = 0u;
-#pragma unroll
-        for (int jj = 0; jj < JR; ++jj) {
-          f.v[jj] = 0.0;
-          f.S[jj] = 0.0;
-          f.lS[jj] = 0.0;
-          if (jb + jj < je) {
-            f.v[jj] = __ldg(p.grp_val + jb + jj);
-            f.S[jj] = group_sum(jb + jj);
-            f.lS[jj] = log(f.S[jj]);
+          return s;
+        };
+        const double sig = hp->sigma[l];
+        const double sig2 = sig * sig;
+        // prior variance sigma_l^2 (normal) or sigma_l^2 xi_gl (xi column)
+        const double inv2v = xcol ? 1.0 / (2.0 * (sig2 * p.xi[so * L * G + i]))
+                                  : 1.0 / (2.0 * sig2);
+        w0 = beta_w[i];
+        w = w0;
+        wa = tuning ? beta_wa[i] : 0.0;
+        Stream rng;
+        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l));
+        if constexpr (JR > 0) {
+          BetaFR<JR> f;
+          f.a = __ldg(p.A + i);
+          f.theta = hp->theta[l];
+          f.inv_two_sig2 = inv2v;
+          f.e700 = p.exp_clamp;
+          f.tab = etab;
+          f.J = je - jb;
+          f.clamps = 0u;
+  #pragma unroll
+          for (int jj = 0; jj < JR; ++jj) {
+            f.v[jj] = 0.0;
+            f.S[jj] = 0.0;
+            f.lS[jj] = 0.0;
+            if (jb + jj < je) {
+              f.v[jj] = __ldg(p.grp_val + jb + jj);
+              f.S[jj] = group_sum(jb + jj);
+              f.lS[jj] = log(f.S[jj]);
+            }
           }
+          bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
+          clamps += f.clamps;
+        } else {
+          for (int j = jb; j < je; ++j) {
+            const double s = group_sum(j);
+            sS[(j - jb) * kGeneThreads + tid] = s;
+            sLogS[(j - jb) * kGeneThreads + tid] = log(s);
+          }
+          BetaF f{__ldg(p.A + i), hp->theta[l], inv2v, p.exp_clamp,
+                  p.grp_val + jb, sS + tid, sLogS + tid, etab, je - jb, 0u};
+          bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
+          clamps += f.clamps;
         }
-        bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
-        clamps += f.clamps;
-      } else {
+      }
+      __syncwarp();
+      if (!alive) continue;
+      if (st) {
+        record_stall(hp, stall_key(5, l, gg, 0), m);
+        alive = false;
+        continue;
+      }
+      beta[i] = bnew;
+      if (tuning) {
+        beta_w[i] = w;
+        beta_wa[i] = wa;
+      }
+      if (bnew != bold) {
         for (int j = jb; j < je; ++j) {
-          const double s = group_sum(j);
-          sS[(j - jb) * kGeneThreads + tid] = s;
-          sLogS[(j - jb) * kGeneThreads + tid] = log(s);
-        }
-        BetaF f{__ldg(p.A + i), hp->theta[l], inv2v, p.exp_clamp,
-                p.grp_val + jb, sS + tid, sLogS + tid, etab, je - jb, 0u};
-        bnew = slice_step(f, bold, w, wa, sc, m, rng, st);
-        clamps += f.clamps;
-      }
-    }
-    __syncwarp();
-    if (!alive) continue;
-    if (st) {
-      record_stall(hp, stall_key(5, l, gg, 0), m);
-      alive = false;
-      continue;
-    }
-    beta[i] = bnew;
-    if (tuning) {
-      beta_w[i] = w;
-      beta_wa[i] = wa;
-    }
-    if (bnew != bold) {
-      for (int j = jb; j < je; ++j) {
-        const double v = __ldg(p.grp_val + j);
-        for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
-          const int n = __ldg(p.grp_mem + q);
-          xs[n * kGeneThreads + tid] += v * (bnew - bold);
+          const double v = __ldg(p.grp_val + j);
+          for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
+            const int n = __ldg(p.grp_mem + q);
+            xs[n * kGeneThreads + tid] += v * (bnew - bold);
+          }
         }
       }
+      if (monitor) moments(p.acc_beta + so * 4 * L * G + i, (size_t)L * G, bnew, mcount);
     }
-    if (monitor) moments(p.acc_beta + so * 4 * L * G + i, (size_t)L * G, bnew, mcount);
-  }
 
-  __syncwarp();
-  if (alive && monitor) {
-    // per-gene contrasts that read only this gene's beta/gamma
-    if (p.ctab_gene_in_sweep) {
-      const ContrastTable* t = p.ctab;
-      const double gam = p.gam[so * G + gl];
-      for (int ci = 0; ci < p.ctab_n; ++ci)
-        if (t->per_gene[ci])
-          contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + p.g0 + gl,
-                          mcount, beta, G, gl, gam, hp);
-    }
-    // thinning of saved genes, P:src/engine.cpp:433-447
-    const long cnt = m - p.burnin;
-    const int sv = p.saved_slot[gl];
-    if (sv >= 0 && cnt % p.thin == 0) {
-      const long row = cnt / p.thin - 1;
-      if (row < p.n_rows) {
-        double* smp = p.samples + so * p.n_cols * p.n_rows;
-        const long c0 = 2 + 2 * (long)L + (long)sv * (L + 1);
-        for (int l = 0; l < L; ++l)
-          smp[(c0 + l) * p.n_rows + row] = beta[(size_t)l * G + gl];
-        smp[(c0 + L) * p.n_rows + row] = p.gam[so * G + gl];
+    __syncwarp();
+    if (alive && monitor) {
+      // per-gene contrasts that read only this gene's beta/gamma
+      if (p.ctab_gene_in_sweep) {
+        const ContrastTable* t = p.ctab;
+        const double gam = p.gam[so * G + gl];
+        for (int ci = 0; ci < p.ctab_n; ++ci)
+          if (t->per_gene[ci])
+            contrast_update(t, ci, p.cprob + so * t->n_prob + t->prob_off[ci] + p.g0 + gl,
+                            mcount, beta, G, gl, gam, hp);
+      }
+      // thinning of saved genes, P:src/engine.cpp:433-447
+      const long cnt = m - p.burnin;
+      const int sv = p.saved_slot[gl];
+      if (sv >= 0 && cnt % p.thin == 0) {
+        const long row = cnt / p.thin - 1;
+        if (row < p.n_rows) {
+          double* smp = p.samples + so * p.n_cols * p.n_rows;
+          const long c0 = 2 + 2 * (long)L + (long)sv * (L + 1);
+          for (int l = 0; l < L; ++l)
+            smp[(c0 + l) * p.n_rows + row] = beta[(size_t)l * G + gl];
+          smp[(c0 + L) * p.n_rows + row] = p.gam[so * G + gl];
+        }
       }
     }
   }
@@ -1068,17 +1075,17 @@ __device__ void gene_leaf_epilogue(const SweepParams& p, int slot, long m, doubl
   }
 }
 
-template <int JR, bool XI>
+template <int JR, bool XI, int PH>
 __global__ void __launch_bounds__(kGeneThreads, CMC_GENE_MIN_BLOCKS)
     gene_sweep_kernel(const SweepParams p, const long m_off) {
   extern __shared__ double smem[];
   __shared__ double exp_tab[32];
   exp_table_init(exp_tab);
   __syncthreads();
-  gene_sweep_body<JR, XI>(p, m_off, smem, ExpTab(exp_tab));
+  gene_sweep_body<JR, XI, PH>(p, m_off, smem, ExpTab(exp_tab));
   // the lp buffer (at least 4 x 128 doubles, gene_sweep_smem_bytes) is free
   // now: it stages the leaf sums
-  if constexpr (!XI) {
+  if constexpr (!XI && (PH & 2) != 0) {
     if (p.fuse_leaf_a) gene_leaf_epilogue<XI>(p, p.slot_base + blockIdx.y, *p.d_m + m_off, smem);
   }
 }
@@ -1099,8 +1106,12 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
     if ((tid & 31) == 0) red[q] = r;
   }
   __syncthreads();
+  // per-step timing mode: SM cycles of each draw (clock64 on the drawing
+  // thread), summed into p.step_cycles[slot][0..2]
+  unsigned long long* cyc = p.step_cycles ? p.step_cycles + 4 * (size_t)slot : nullptr;
   if (tid == 0) {
     const double s1 = red[0], s2 = red[1];
+    const long long c0 = clock64();
     // Step 3: nu, P:src/engine.cpp:228-248
     {
       NuF f{Gd, hp->tau, s1, s2, p.d};
@@ -1120,6 +1131,8 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
       hp->w_nu = w;
       hp->wa_nu = wa;
     }
+    const long long c1 = clock64();
+    if (cyc) cyc[0] += (unsigned long long)(c1 - c0);
     // Step 4: tau, P:src/engine.cpp:250-267 / P:src/model.cpp:102-105
     {
       const double nu = hp->nu;
@@ -1146,8 +1159,10 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
         hp->wa_tau = wa;
       }
     }
+    if (cyc) cyc[1] += (unsigned long long)(clock64() - c1);
   } else if (tid >= 32 && tid < 32 + L) {
     // Step 6: theta_l, P:src/engine.cpp:336-347 / P:src/model.cpp:124-129
+    const long long c0 = clock64();
     const int l = tid - 32;
     const double sb = red[2 + l];
     const double sg = hp->sigma[l], c = p.c[l];
@@ -1160,6 +1175,7 @@ __device__ void hyper_a_body(const SweepParams& p, int slot, long m) {
     Stream rng;
     rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteTheta, l));
     hp->theta[l] = mean + sd * normal(rng);
+    if (cyc && l == 0) cyc[2] += (unsigned long long)(clock64() - c0);
   }
 }
 
@@ -1427,13 +1443,17 @@ cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
 template <int JR, bool XI>
 static cudaError_t raise_smem(int dyn, int optin, int* total) {
   cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, gene_sweep_kernel<JR, XI>);
+  cudaError_t e = cudaFuncGetAttributes(&fa, gene_sweep_kernel<JR, XI, 3>);
   if (e != cudaSuccess) return e;
   *total = (int)fa.sharedSizeBytes + dyn;
   if (*total > optin) return cudaSuccess;  // the caller reports CMC_ERR_CONFIG
-  if (dyn > fa.maxDynamicSharedSizeBytes)
-    e = cudaFuncSetAttribute(gene_sweep_kernel<JR, XI>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if (dyn > fa.maxDynamicSharedSizeBytes) {
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if ((e = cudaFuncSetAttribute(gene_sweep_kernel<JR, XI, 3>, attr, dyn)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(gene_sweep_kernel<JR, XI, 1>, attr, dyn)) != cudaSuccess)
+      return e;
+    e = cudaFuncSetAttribute(gene_sweep_kernel<JR, XI, 2>, attr, dyn);
+  }
   return e;
 }
 
@@ -1458,21 +1478,27 @@ cudaError_t configure_gene_kernels(int N, int Jmax, int xi_any, int* total) {
 
 template <int JR, bool XI>
 static cudaError_t launch_gene_sweep_t(const SweepParams& p, int chains, long m_off,
-                                       cudaStream_t s) {
+                                       cudaStream_t s, int phase) {
   const int smem = gene_sweep_smem_bytes(p.N, JR > 0 ? 0 : p.Jmax);
   dim3 grid((unsigned)((p.G + kGeneThreads - 1) / kGeneThreads), (unsigned)chains);
-  return launch_prio(gene_sweep_kernel<JR, XI>, grid, dim3(kGeneThreads), smem, s, p.prio_gene, p,
-                     m_off);
+  if (phase == 1)
+    return launch_prio(gene_sweep_kernel<JR, XI, 1>, grid, dim3(kGeneThreads), smem, s,
+                       p.prio_gene, p, m_off);
+  if (phase == 2)
+    return launch_prio(gene_sweep_kernel<JR, XI, 2>, grid, dim3(kGeneThreads), smem, s,
+                       p.prio_gene, p, m_off);
+  return launch_prio(gene_sweep_kernel<JR, XI, 3>, grid, dim3(kGeneThreads), smem, s,
+                     p.prio_gene, p, m_off);
 }
 
 cudaError_t launch_gene_sweep(const SweepParams& p, int chains, long m_off,
-                              cudaStream_t s) {
+                              cudaStream_t s, int phase) {
   if (p.xi_any) {
-    if (p.Jmax <= 2) return launch_gene_sweep_t<2, true>(p, chains, m_off, s);
-    return launch_gene_sweep_t<0, true>(p, chains, m_off, s);
+    if (p.Jmax <= 2) return launch_gene_sweep_t<2, true>(p, chains, m_off, s, phase);
+    return launch_gene_sweep_t<0, true>(p, chains, m_off, s, phase);
   }
-  if (p.Jmax <= 2) return launch_gene_sweep_t<2, false>(p, chains, m_off, s);
-  return launch_gene_sweep_t<0, false>(p, chains, m_off, s);
+  if (p.Jmax <= 2) return launch_gene_sweep_t<2, false>(p, chains, m_off, s, phase);
+  return launch_gene_sweep_t<0, false>(p, chains, m_off, s, phase);
 }
 
 // Layout transposes for state/output transfer: SoA [K][G] <-> the

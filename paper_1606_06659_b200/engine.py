@@ -462,6 +462,14 @@ class GibbsEngine:
         self._lib.cmc_shard_bounds(self.G, rank, world, byref(lo), byref(hi))
         self.shard_range = (lo.value, hi.value)
 
+    def set_step_timing(self, on: bool = True):
+        """Per-step timing mode (debug): sweeps launch each of the seven
+        steps on its own with CUDA events between them, and the outputs'
+        step_seconds hold per-step device seconds (reference StepTimings,
+        P:src/engine.cpp:173-176).  Bit-identical results, slower sweeps;
+        single GPU."""
+        self._lib.cmc_engine_set_step_timing(self._h, 1 if on else 0)
+
     def shard_loopback(self, rank: int, group: "LoopbackGroup"):
         """Test hook: join an in-process loopback group as `rank` instead of
         an NCCL clique (cmc_engine_shard_loopback).  Each engine of the

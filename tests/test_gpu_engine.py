@@ -248,3 +248,27 @@ def test_iterate_after_run_leaves_the_run_untouched():
     keep = np.ones(len(p), bool)
     keep[th] = False
     assert not len(mismatch(p[keep], ost[keep]))
+
+
+def test_step_timing_mode_is_bit_identical_and_reports_every_step():
+    """The per-step timing mode (reference StepTimings,
+    P:src/engine.cpp:173-176): each step launched on its own with events
+    between them.  Same results bit for bit; every one of the seven steps
+    gets device time (the reference's step order: epsilon, gamma, nu, tau,
+    beta, theta, sigma)."""
+    counts, X, h = heterosis(3000, seed=5)
+    cfg = RunConfig(chains=2, burnin=20, iterations=20, thin=5, seed=9, save_genes=5)
+    a = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg,
+                    contrasts=[heterosis_contrast()]).run()
+    eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg, contrasts=[heterosis_contrast()])
+    eng.set_step_timing(True)
+    b = eng.run()
+    for c in range(2):
+        assert np.array_equal(a[c].final_state.pack(), b[c].final_state.pack())
+        assert np.array_equal(a[c].beta_acc.mean, b[c].beta_acc.mean)
+        assert np.array_equal(a[c].samples, b[c].samples)
+        assert np.array_equal(a[c].contrasts[0].prob, b[c].contrasts[0].prob)
+        st = b[c].step_seconds
+        assert st.shape == (7,) and np.all(st > 0), st
+        # the fused schedule reports one device time under the first step
+        assert a[c].step_seconds[0] > 0 and np.all(a[c].step_seconds[1:] == 0)

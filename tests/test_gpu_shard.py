@@ -85,3 +85,21 @@ def test_exchange_path_two_lanes_with_xi_prior():
         assert np.array_equal(a[c].xi_acc.mean, b[c].xi_acc.mean)
         assert np.array_equal(a[c].sigma_acc.mean, b[c].sigma_acc.mean)
         assert np.array_equal(a[c].contrasts[0].prob, b[c].contrasts[0].prob)
+
+
+def test_exchange_path_stall_equals_fused_path():
+    """A stall on the NCCL path: the stall flag goes through the gathered
+    partials and the records through the sync-time ncclAllGather of stall
+    records; the error equals the fused engine's (and so the reference's
+    first stall, tests/test_gpu_parity.py)."""
+    from paper_1606_06659_b200 import SamplerStallError
+    counts, X, h = heterosis(2500, seed=4)
+    cfg = RunConfig(chains=2, burnin=30, iterations=30, thin=10, seed=5)
+    cfg.slice.max_shrink = 2
+    fused, shard = engines(counts, X, h, cfg)
+    with pytest.raises(SamplerStallError) as a:
+        fused.run()
+    with pytest.raises(SamplerStallError) as b:
+        shard.run()
+    assert str(a.value) == str(b.value)
+    assert (a.value.x0, a.value.width) == (b.value.x0, b.value.width)

@@ -148,3 +148,67 @@ def test_two_lane_sections_are_bit_exact(G):
     r0, f0 = out[0]
     r1, f1 = out[1]
     assert r0 == r1 == f0 == f1, "per-lane sharded reduction differs from det_transform_sum"
+
+
+def ordered_lanes_worker(rank, world, port, sweeps, out):
+    """engine.cu enqueue_sweep_on's collective order on 2 ranks: each chain
+    lane runs on its own host thread (its own stream), and every all-gather
+    first waits for the collective enqueued before it (ev_coll: lane 0's A
+    and B, then lane 1's A and B, then the next sweep), so every rank issues
+    the gathers in one order.  Here both lanes share ONE process group (the
+    strictest case: a communicator needs the same issue order everywhere);
+    rank 1 starts its lanes in reverse order with staggered delays, and every
+    gathered section must still hold the right lane's, sweep's and phase's
+    data."""
+    import threading
+    import time
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lanes = 2
+    # the chain of events: slot k of the global order completes -> k + 1 may go
+    order = [(s, lane, ph) for s in range(sweeps) for lane in range(lanes) for ph in "AB"]
+    done = [threading.Event() for _ in order]
+    got = {}
+    errs = []
+
+    def lane_thread(lane):
+        try:
+            for k, (s, ln, ph) in enumerate(order):
+                if ln != lane:
+                    continue
+                if k > 0:
+                    done[k - 1].wait(timeout=60)   # cudaStreamWaitEvent(t, ev_coll)
+                mine = torch.tensor([float(rank), float(lane), float(s), float(ph == "B")],
+                                    dtype=torch.float64)
+                buf = torch.zeros(world * 4, dtype=torch.float64)
+                dist.all_gather_into_tensor(buf, mine)
+                got[(s, lane, ph)] = buf.view(world, 4).numpy().copy()
+                done[k].set()                        # cudaEventRecord(ev_coll, t)
+        except Exception as ex:  # reported below
+            errs.append(repr(ex))
+
+    ts = [threading.Thread(target=lane_thread, args=(ln,), daemon=True) for ln in range(lanes)]
+    starts = list(range(lanes)) if rank == 0 else list(reversed(range(lanes)))
+    for i, ln in enumerate(starts):
+        ts[ln].start()
+        time.sleep(0.05 * (i + rank))
+    for t in ts:
+        t.join(timeout=120)
+    ok = not errs and all(not t.is_alive() for t in ts) and len(got) == len(order)
+    if ok:
+        for (s, lane, ph), g in got.items():
+            want = np.array([[r, lane, s, float(ph == "B")] for r in range(world)])
+            ok &= np.array_equal(g, want)
+    out[rank] = (ok, errs)
+    dist.destroy_process_group()
+
+
+def test_collective_order_across_lanes_is_rank_independent():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(ordered_lanes_worker, args=(world, free_port(), 4, out), nprocs=world, join=True)
+    for r in range(world):
+        ok, errs = out[r]
+        assert ok, (r, errs)
