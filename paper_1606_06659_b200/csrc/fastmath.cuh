@@ -69,9 +69,23 @@ __device__ __forceinline__ double fast_exp_le700(double x, const ExpTab tab) {
   return __hiloint2double(__double2hiint(res) + ((k >> 5) << 20), __double2loint(res));
 }
 
+// the table path's range [-707, 700] as one predicate: one branch per call
+// (1% of the sweep against two tests, A/B on B200)
 __device__ __forceinline__ double fast_exp(double x, const ExpTab tab) {
-  if (x > 700.0) return exp(x);
-  return fast_exp_le700(x, tab);
+  if (!((x >= -707.0) & (x <= 700.0))) return exp(x);
+  const double t = fma(x, kExpC[0], kExpC[1]);
+  const int k = __double2loint(t);
+  const double kd = t - kExpC[1];
+  double r = fma(kd, -kExpC[2], x);
+  r = fma(kd, -kExpC[3], r);
+  double s = fma(r, kExpC[4], kExpC[5]);
+  s = fma(s, r, kExpC[6]);
+  s = fma(s, r, kExpC[7]);
+  s = fma(s, r, 0.5);
+  const double p = fma(s, r * r, r);
+  const double tj = tab[k & 31];
+  const double res = fma(tj, p, tj);
+  return __hiloint2double(__double2hiint(res) + ((k >> 5) << 20), __double2loint(res));
 }
 
 }  // namespace cmc
