@@ -530,6 +530,10 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.partB = e->partB.p;
   p.C = (int)C;
   p.xi_any = e->xi_any ? 1 : 0;
+  {
+    const char* v = std::getenv("CMC_XI_TRIPS");  // development override (A/B)
+    p.xi_trips = v ? std::atoi(v) : 16;
+  }
   for (long l = 0; l < L; ++l) p.xi_fam[l] = e->prior[(size_t)l];
   p.t_df = e->t_df;
   p.xi = e->xi.p;

@@ -150,6 +150,7 @@ struct SweepParams {
   // 1/gamma, S_l, W_l] with S_l = sum beta_l (normal column) or sum
   // beta_l/xi_l, and W_l = sum 1/xi_l; partB holds sum (beta-theta)^2[/xi].
   int xi_any;
+  int xi_trips;       // xi kernel: slice trips before the straggling lanes are parked
   int xi_fam[kLMax];  // CMC_PRIOR_* per column
   double t_df;
   double *xi, *xi_w, *xi_wa;  // [C][L][G]

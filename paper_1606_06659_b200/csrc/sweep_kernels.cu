@@ -119,6 +119,88 @@ __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
   return x1;
 }
 
+// slice_step as a resumable state machine (same draws, same evaluation
+// order, same trip body): start() draws log u, the placement and K_L;
+// trips() runs at most `max_trips` trips and reports running / accepted /
+// stalled; finish() applies the tuning update.  A lane's whole state
+// (SliceRun + the Stream queue) can be parked in shared memory after a
+// bounded first pass and resumed by another thread (xi_sweep_kernel).
+struct SliceRun {
+  double x0, logu, lo, hi, x1, wv;
+  int kl, kr, phase, it;
+};
+enum : int { kSliceRunning = 0, kSliceAccepted = 1, kSliceStalled = 2 };
+
+template <class F>
+__device__ __forceinline__ void slice_start(F& f, double x0, double w, const SliceCfg& sc,
+                                            Stream& rng, SliceRun& s) {
+  const double fx0 = f(x0);
+  s.x0 = x0;
+  s.logu = fx0 + log(rng.u01());
+  s.wv = w;
+  s.lo = x0 - w * rng.u01();
+  s.hi = s.lo + w;
+  const int kl0 = (int)rng.uniform_int_pre((uint64_t)sc.K + 1, sc.reject_below, sc.inv);
+  s.kl = kl0;
+  s.kr = sc.K - kl0;
+  s.phase = s.kl > 0 ? 0 : (s.kr > 0 ? 1 : 2);
+  s.it = 0;
+  s.x1 = x0;
+}
+
+template <class F>
+__device__ __forceinline__ int slice_trips(F& f, const SliceCfg& sc, Stream& rng, SliceRun& s,
+                                           int max_trips) {
+  double lo = s.lo, hi = s.hi, x1 = s.x1;
+  int kl = s.kl, kr = s.kr, phase = s.phase, it = s.it;
+  const double wv = s.wv, logu = s.logu, x0 = s.x0;
+  int res = kSliceRunning;
+  for (int trip = 0; trip < max_trips; ++trip) {
+    const bool S = phase == 2;
+    if (S && rng.na == 0) rng.refill();
+    const double u = ((double)(rng.a0 >> 11) + 0.5) * 0x1.0p-53;
+    if (S) {
+      rng.a0 = rng.a1;
+      rng.a1 = rng.a2;
+      rng.a2 = rng.a3;
+      --rng.na;
+    }
+    const double xs = lo + (hi - lo) * u;
+    const double xe = S ? xs : (phase == 0 ? lo : hi);
+    const double fe = f(xe);
+    const bool Lp = phase == 0, Rp = phase == 1;
+    const bool in = logu < fe;
+    const bool acc = S && (fe > logu);
+    const bool rej = S && !(fe > logu);
+    lo = (Lp && in) ? lo - wv : lo;
+    hi = (Rp && in) ? hi + wv : hi;
+    kl -= (Lp && in) ? 1 : 0;
+    kr -= (Rp && in) ? 1 : 0;
+    hi = (rej && xs > x0) ? xs : hi;
+    lo = (rej && !(xs > x0)) ? xs : lo;
+    it += rej ? 1 : 0;
+    x1 = S ? xs : x1;
+    const int after_l = kr > 0 ? 1 : 2;
+    phase = (Lp && !(in && kl > 0)) ? after_l : ((Rp && !(in && kr > 0)) ? 2 : phase);
+    if (acc) {
+      res = kSliceAccepted;
+      break;
+    }
+    if (it >= sc.max_shrink) {
+      res = kSliceStalled;
+      break;
+    }
+  }
+  s.lo = lo;
+  s.hi = hi;
+  s.x1 = x1;
+  s.kl = kl;
+  s.kr = kr;
+  s.phase = phase;
+  s.it = it;
+  return res;
+}
+
 // Two-phase slice step for log densities whose exp terms are exp(v x + c):
 // the step-out evaluation points move by exactly -w (left) / +w (right)
 // and the step-out draws no random numbers, so (1) both sides step out in
@@ -847,6 +929,9 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
 #ifndef CMC_XI_MIN_BLOCKS
 #define CMC_XI_MIN_BLOCKS 8
 #endif
+#ifndef CMC_XI_PARK_MIN_BLOCKS
+#define CMC_XI_PARK_MIN_BLOCKS 6
+#endif
 __global__ void __launch_bounds__(kGeneBlock, CMC_XI_MIN_BLOCKS)
     xi_sweep_kernel(const SweepParams p, const long m_off) {
   const int l = blockIdx.y;
@@ -887,6 +972,116 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_MIN_BLOCKS)
   if (p.monitor_enabled && m > p.burnin)
     moments(p.acc_xi + so * 4 * L * G + (size_t)l * G + gl, (size_t)L * G, x1,
             (double)(m - p.burnin));
+}
+
+// The same step for a launch with a horseshoe column (xi_park_kernel).
+// Divergence: a horseshoe xi's slice loop is heavy-tailed (long step-outs,
+// many shrinks), and a warp runs as long as its slowest lane.  So the loop
+// runs at most p.xi_trips trips for every lane (the warp-level vote of
+// __syncthreads_count decides whether any lane is left), then every lane
+// still running parks its whole state (slice state, Philox queue, density
+// parameter) in shared memory, and the block's first threads resume the
+// parked steps densely packed, one per thread.  The continuation draws the
+// same uniforms in the same order, so the result is unchanged.
+struct XiParked {
+  SliceRun s;
+  uint64_t a0, a1, a2, a3, b0, b1, b2, b3;
+  double q, w, wa;
+  unsigned block, na, nb;
+  int gl;
+};
+constexpr int kXiPark = kGeneBlock;  // every lane of the block can park
+
+__global__ void __launch_bounds__(kGeneBlock, CMC_XI_PARK_MIN_BLOCKS)
+    xi_park_kernel(const SweepParams p, const long m_off) {
+  __shared__ XiParked park[kXiPark];
+  __shared__ int n_park;
+  const int l = blockIdx.y;
+  if (p.xi_fam[l] == CMC_PRIOR_NORMAL) return;  // block-uniform
+  const int slot = p.slot_base + blockIdx.z;
+  Hyper* hp = p.hyper + slot;
+  if (threadIdx.x == 0) n_park = stalled_chain(hp) ? -1 : 0;
+  __syncthreads();
+  if (n_park < 0) return;  // block-uniform
+  const long gl = (long)blockIdx.x * kGeneBlock + threadIdx.x;
+  const bool alive = gl < p.G;
+  const long m = *p.d_m + m_off;
+  const bool tuning = m <= p.burnin;
+  const int L = p.L;
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const uint64_t chain = (uint64_t)(p.chain_base + blockIdx.z);
+  const SliceCfg sc{p.K, p.max_shrink, p.burnin, p.tune_cutoff, p.k_reject, p.k_inv};
+  const double sg = hp->sigma[l];
+  const double th = hp->theta[l];
+  const bool monitor = p.monitor_enabled && m > p.burnin;
+  // result of one lane's step (pass 1 or resumed): xi, width, stall
+  auto finish = [&](long g, int res, const SliceRun& s, double w, double wa) {
+    const size_t ix = so * L * G + (size_t)l * G + g;
+    if (res == kSliceStalled) {
+      record_stall(hp, stall_key(5, l, (uint64_t)(p.g0 + g), 1), m);
+      return;
+    }
+    if (m <= sc.burnin) tune_update(w, wa, m, fabs(s.x1 - s.x0), sc.tune_cutoff);
+    p.xi[ix] = s.x1;
+    if (tuning) {
+      p.xi_w[ix] = w;
+      p.xi_wa[ix] = wa;
+    }
+    if (monitor)
+      moments(p.acc_xi + so * 4 * L * G + (size_t)l * G + g, (size_t)L * G, s.x1,
+              (double)(m - p.burnin));
+  };
+  int res = kSliceAccepted;
+  SliceRun s;
+  Stream rng;
+  double w = 0.0, wa = 0.0, q = 0.0;
+  if (alive) {
+    const size_t ix = so * L * G + (size_t)l * G + gl;
+    const double dz = p.beta[ix] - th;
+    q = dz * dz / (2.0 * (sg * sg));
+    XiF f{p.xi_fam[l], q, p.t_df};
+    w = p.xi_w[ix];
+    wa = tuning ? p.xi_wa[ix] : 0.0;
+    rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteXi, (uint64_t)(p.g0 + gl) * L + l));
+    slice_start(f, p.xi[ix], w, sc, rng, s);
+    res = slice_trips(f, sc, rng, s, p.xi_trips);
+  }
+  // park the lanes still running
+  const bool parked = alive && res == kSliceRunning;
+  if (parked) {
+    const int k = atomicAdd(&n_park, 1);
+    {
+      XiParked& e = park[k];
+      e.s = s;
+      e.a0 = rng.a0; e.a1 = rng.a1; e.a2 = rng.a2; e.a3 = rng.a3;
+      e.b0 = rng.b0; e.b1 = rng.b1; e.b2 = rng.b2; e.b3 = rng.b3;
+      e.block = rng.block; e.na = rng.na; e.nb = rng.nb;
+      e.q = q;
+      e.w = w;
+      e.wa = wa;
+      e.gl = (int)gl;
+    }
+  }
+  __syncwarp();
+  if (alive && !parked) finish(gl, res, s, w, wa);
+  __syncthreads();
+  const int np = n_park;
+  if ((int)threadIdx.x >= np) return;
+  // resume one parked step per thread, densely packed in the first warps
+  const XiParked& e = park[threadIdx.x];
+  SliceRun r = e.s;
+  Stream rs;
+  rs.k0 = p.seed;
+  rs.k1 = chain;
+  rs.it = (uint64_t)m;
+  rs.site = site_id(kSiteXi, (uint64_t)(p.g0 + e.gl) * L + l);
+  rs.a0 = e.a0; rs.a1 = e.a1; rs.a2 = e.a2; rs.a3 = e.a3;
+  rs.b0 = e.b0; rs.b1 = e.b1; rs.b2 = e.b2; rs.b3 = e.b3;
+  rs.block = e.block; rs.na = e.na; rs.nb = e.nb;
+  XiF f{p.xi_fam[l], e.q, p.t_df};
+  const int rr = slice_trips(f, sc, rs, r, 0x7fffffff);
+  __syncwarp(__activemask());
+  finish(e.gl, rr, r, e.w, e.wa);
 }
 
 // Serial sum of value(i), i in [start, end), from +0.0 in index order: the
@@ -1556,6 +1751,12 @@ cudaError_t launch_transpose(const double* src, double* dst, long G, int K, bool
 cudaError_t launch_xi_sweep(const SweepParams& p, int chains, long m_off,
                             cudaStream_t s) {
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)p.L, (unsigned)chains);
+  // parking pays for the heavy-tailed horseshoe loops only (A/B on B200,
+  // DESIGN.md section 4): horseshoe 1.024 -> 0.950 ms per 4-chain sweep,
+  // t 0.523 -> 0.548 with it
+  bool hs = false;
+  for (int l = 0; l < p.L; ++l) hs |= p.xi_fam[l] == CMC_PRIOR_HORSESHOE;
+  if (hs) return launch_prio(xi_park_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_gene, p, m_off);
   return launch_prio(xi_sweep_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_gene, p, m_off);
 }
 

@@ -118,3 +118,20 @@ def test_python_api_with_laplace_prior():
     st, tu = eng.initial_state(1), eng.tuning_state()
     eng.iterate(st, tu, 1, 1)
     assert st.xi is not None and np.all(st.xi > 0)
+
+
+@pytest.mark.parametrize("trips", ["0", "1", "3"])
+def test_parked_horseshoe_steps_resume_bitwise(trips, monkeypatch):
+    """xi_park_kernel: with a small first-pass trip budget nearly every
+    horseshoe lane parks its slice state and Philox queue in shared memory
+    and is resumed by another thread; the sweeps stay bit-identical to the
+    oracle (burn-in and steady state, a mixed design included)."""
+    monkeypatch.setenv("CMC_XI_TRIPS", trips)
+    for prior in (["horseshoe"], ["normal", "laplace", "t", "horseshoe", "laplace"]):
+        orc, gpu, G, N, L = _pair(prior, G=700, burnin=20)
+        st, tw, ta = packed_start(orc, 1)
+        g = [st.copy(), tw.copy(), ta.copy()]
+        for m in list(range(1, 6)) + [25, 26]:
+            assert orc.iterate(st, tw, ta, 1, m) == gpu.iterate(*g, 1, m)
+            _state_parity(g[0], st, G, N, L, f"{prior} trips={trips} m={m}")
+            assert not len(mismatch(g[1], tw)) and not len(mismatch(g[2], ta))
