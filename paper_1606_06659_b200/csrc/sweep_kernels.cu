@@ -1050,6 +1050,9 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_PARK_MIN_BLOCKS)
   const bool parked = alive && res == kSliceRunning;
   if (parked) {
     const int k = atomicAdd(&n_park, 1);
+#ifdef CMC_DEBUG_BOUNDS
+    assert(k >= 0 && k < kXiPark);
+#endif
     {
       XiParked& e = park[k];
       e.s = s;
@@ -1218,6 +1221,9 @@ __device__ void leaf_a_sums(const SweepParams& p, int slot, long lb, double* sta
       const double* xs = p.xi + so * L * G + (size_t)(q - 2 - L) * G;
       s = warp_serial_sum([&](long i) { return 1.0 / __ldcg(xs + i); }, start, end, buf);
     }
+#ifdef CMC_DEBUG_BOUNDS
+    assert(rank >= 0 && rank < p.world && slot - p.slot_base < p.C && q < Qs && lb < lpr);
+#endif
     if (lane == 0) p.partA[((rank * p.C + (slot - p.slot_base)) * Qs + q) * lpr + lb] = s;
   }
 }
@@ -1228,6 +1234,9 @@ __device__ __forceinline__ void write_stall_flag(const SweepParams& p, int slot,
   const long lpr = p.leaves_per_rank;
   const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
   const int Q = leaf_q_a(p.L, p.xi_any), Qs = leaf_qs_a(p.L, p.xi_any);
+#ifdef CMC_DEBUG_BOUNDS
+  assert(rank >= 0 && rank < p.world && slot - p.slot_base < p.C);
+#endif
   p.partA[((rank * p.C + (slot - p.slot_base)) * Qs + Q) * lpr] = st ? 1.0 : 0.0;
 }
 
@@ -1248,6 +1257,9 @@ __device__ void gene_leaf_epilogue(const SweepParams& p, int slot, long m, doubl
   __syncthreads();
   if (tid == 0) {
     const unsigned nb = min((unsigned)kBlocksPerLeaf, gridDim.x - (unsigned)lb * kBlocksPerLeaf);
+#ifdef CMC_DEBUG_BOUNDS
+    assert(lb < p.n_leaves_local && nb >= 1 && nb <= (unsigned)kBlocksPerLeaf);
+#endif
     unsigned* cnt = p.leaf_cnt + (size_t)slot * p.n_leaves_local + lb;
     const bool last = atomicAdd(cnt, 1u) == nb - 1;
     if (last) *cnt = 0;
@@ -1550,6 +1562,9 @@ __global__ void __launch_bounds__(32 * kTailWarps) leaf_b_kernel(const SweepPara
     if (lane == 0) {
       const long lpr = p.leaves_per_rank;
       const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
+#ifdef CMC_DEBUG_BOUNDS
+      assert(rank >= 0 && rank < p.world && slot - p.slot_base < p.C && lb < lpr);
+#endif
       p.partB[((rank * p.C + (slot - p.slot_base)) * L + q) * lpr + lb] = s;
     }
   }
