@@ -547,7 +547,10 @@ __device__ __forceinline__ PartView part_view(const double* part, const SweepPar
   return PartView{part, p.C, slot - p.slot_base, Q, p.leaves_per_rank};
 }
 __device__ __forceinline__ double leaf_part(const PartView& v, int q, long leaf) {
-  const long r = leaf / v.lpr, j = leaf % v.lpr;
+  // leaf counts fit 32 bits (< 2^22 leaves at G < 2^32): a 32-bit division
+  // (round 1's 64-bit one was a ~100-instruction subroutine call per leaf)
+  const unsigned lpr = (unsigned)v.lpr;
+  const long r = (unsigned)leaf / lpr, j = (unsigned)leaf - (unsigned)r * lpr;
 #ifdef CMC_DEBUG_BOUNDS
   assert(v.c >= 0 && v.c < v.C && q < v.Q);
 #endif
@@ -1146,8 +1149,8 @@ __device__ __forceinline__ double pairwise_fixed(const PartView& v, int q, long 
 
 // pairwise_sum of one quantity's leaf partials by one warp.  Lane k walks
 // the top five midpoint splits along the bits of k, sums its depth-5
-// subtree with the same recursion (straight-line up to 64 leaves per lane,
-// i.e. 2,048 leaves = 2M genes; the plain recursion beyond), and the 31
+// subtree with the same recursion (straight-line up to 32 leaves per lane,
+// i.e. 1,024 leaves = 1M genes; the plain recursion beyond), and the 31
 // internal nodes above are rebuilt with shuffles as left + right.  A node
 // of size 1 passes its single leaf through and a node of size 0 is 0.0, as
 // the reference recursion returns them, so the result is bit-identical.
@@ -1166,7 +1169,7 @@ __device__ double warp_pairwise_leaves(const PartView pv, int q, int n) {
       cnt = mid;
     }
   }
-  const double v0 = cnt <= 64 ? pairwise_fixed<64>(pv, q, lo, cnt) : pairwise_leaves(pv, q, lo, cnt);
+  const double v0 = cnt <= 32 ? pairwise_fixed<32>(pv, q, lo, cnt) : pairwise_leaves(pv, q, lo, cnt);
   double v = v0;
 #pragma unroll
   for (int d = 4; d >= 0; --d) {
