@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--burnin", type=int, default=200)
     ap.add_argument("--e2e-burnin", type=int, default=2000)      # reference RunConfig default
     ap.add_argument("--e2e-iterations", type=int, default=4000)  # reference RunConfig default
-    ap.add_argument("--e2e-reps", type=int, default=2)  # complete runs; the fastest is reported
+    ap.add_argument("--e2e-reps", type=int, default=3)  # complete runs; the fastest is reported
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-min-sweeps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")

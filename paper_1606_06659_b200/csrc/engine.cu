@@ -1532,11 +1532,40 @@ int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
   const long XI = e->xi_any ? e->G_total * e->L : 0;
   const long S = e->G_total * e->N + e->G_total + e->G_total * e->L + 2 * e->L + 2 + XI;
   const long T = e->G_total * e->N + e->G_total + e->G_total * e->L + e->L + 2 + XI;
-  std::vector<double> st((size_t)S), tw((size_t)T, e->cfg.w_init), ta((size_t)T, 0.0);
+  (void)T;
+  std::vector<double> st((size_t)S);
   CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * e->C));
   for (long c = 0; c < e->C; ++c) {
     initial_state_host(e, c, st.data());
-    if ((rc = upload_state(e, c, st.data(), tw.data(), ta.data(), err))) return rc;
+    if ((rc = upload_state(e, c, st.data(), nullptr, nullptr, err))) return rc;
+  }
+  // fresh tuning of every run chain (TuningState(G, N, L, w_init),
+  // P:include/countmc/engine.hpp:58-74): widths w_init, accumulators 0,
+  // filled on the device instead of uploading two packed host arrays
+  {
+    const size_t C = (size_t)e->C, G = (size_t)e->G, N = (size_t)e->N, L = (size_t)e->L;
+    const double w0 = e->cfg.w_init;
+    CUDA_TRY(launch_fill(e->eps_w.p, C * N * G, w0, e->stream));
+    CUDA_TRY(launch_fill(e->gam_w.p, C * G, w0, e->stream));
+    CUDA_TRY(launch_fill(e->beta_w.p, C * L * G, w0, e->stream));
+    CUDA_TRY(cudaMemsetAsync(e->eps_wa.p, 0, sizeof(double) * C * N * G, e->stream));
+    CUDA_TRY(cudaMemsetAsync(e->gam_wa.p, 0, sizeof(double) * C * G, e->stream));
+    CUDA_TRY(cudaMemsetAsync(e->beta_wa.p, 0, sizeof(double) * C * L * G, e->stream));
+    if (e->xi_any) {
+      CUDA_TRY(launch_fill(e->xi_w.p, C * L * G, w0, e->stream));
+      CUDA_TRY(cudaMemsetAsync(e->xi_wa.p, 0, sizeof(double) * C * L * G, e->stream));
+    }
+    std::vector<Hyper> hp(C);
+    CUDA_TRY(cudaMemcpy(hp.data(), e->hyper.p, sizeof(Hyper) * C, cudaMemcpyDeviceToHost));
+    for (auto& h : hp) {
+      for (long l = 0; l < e->L; ++l) {
+        h.w_sigma[l] = w0;
+        h.wa_sigma[l] = 0.0;
+      }
+      h.w_nu = h.w_tau = w0;
+      h.wa_nu = h.wa_tau = 0.0;
+    }
+    CUDA_TRY(cudaMemcpy(e->hyper.p, hp.data(), sizeof(Hyper) * C, cudaMemcpyHostToDevice));
   }
   CUDA_TRY(cudaMemset(e->acc_eps.p, 0, sizeof(double) * e->acc_eps.n));
   CUDA_TRY(cudaMemset(e->acc_gam.p, 0, sizeof(double) * e->acc_gam.n));

@@ -185,6 +185,7 @@ cudaError_t launch_hyper_b(const SweepParams& p, int chains, long m_off,
 cudaError_t launch_gene_contrast(const SweepParams& p, int chains, long m_off,
                                  cudaStream_t s);
 cudaError_t launch_advance(long* d_m, long by, cudaStream_t s);
+cudaError_t launch_fill(double* p, size_t n, double v, cudaStream_t s);
 cudaError_t launch_fastmath_setup(cudaStream_t s);
 cudaError_t launch_compute_A(const double* y, const double* X, double* A,
                              int G, int N, int L, cudaStream_t s);

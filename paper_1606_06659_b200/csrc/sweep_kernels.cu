@@ -1607,6 +1607,12 @@ __global__ void gene_contrast_kernel(const SweepParams p, const long m_off) {
 
 __global__ void advance_kernel(long* d_m, long by) { *d_m += by; }
 
+__global__ void fill_kernel(double* p, size_t n, double v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
 // A_gl = sum_n y_gn X_nl accumulated in n order, P:src/engine.cpp:55-60.
 __global__ void compute_A_kernel(const double* y, const double* X, double* A,
                                  int G, int N, int L) {
@@ -1825,6 +1831,13 @@ cudaError_t launch_gene_contrast(const SweepParams& p, int chains, long m_off,
 
 cudaError_t launch_fastmath_setup(cudaStream_t s) {
   fastmath_setup_kernel<<<1, 32, 0, s>>>();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(double* p, size_t n, double v, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const size_t blocks = std::min<size_t>((n + 255) / 256, 148 * 16);
+  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, n, v);
   return cudaGetLastError();
 }
 
