@@ -1,8 +1,9 @@
 #!/bin/bash
-# A/B of xi-prior sweep timings over library builds and CMC_XI_TRIPS values
+# A/B of xi-prior sweep timings over library builds in exp/ (and CMC_XI_TRIPS)
 for rep in 1 2; do
-  echo "== base (rep $rep)"; CMC_LIB_OVERRIDE=$PWD/exp/xi_base.so python scripts/xi_time.py horseshoe t
-  for T in 4 8 16 32; do
-    echo "== park T=$T (rep $rep)"; CMC_XI_TRIPS=$T CMC_LIB_OVERRIDE=$PWD/exp/xi_park.so python scripts/xi_time.py horseshoe t
+  for lib in "$@"; do
+    for T in ${TRIPS:-16}; do
+      echo "== $lib T=$T (rep $rep)"; CMC_XI_TRIPS=$T CMC_LIB_OVERRIDE=$PWD/$lib python scripts/xi_time.py horseshoe t
+    done
   done
 done
