@@ -272,3 +272,36 @@ def test_step_timing_mode_is_bit_identical_and_reports_every_step():
         assert st.shape == (7,) and np.all(st > 0), st
         # the fused schedule reports one device time under the first step
         assert a[c].step_seconds[0] > 0 and np.all(a[c].step_seconds[1:] == 0)
+
+
+def test_sweep_calls_of_any_length_replay_the_same_sweeps():
+    """cmc_engine_sweeps replays every sweep from a CUDA graph of the call's
+    length (whole 50-sweep graphs plus one of the remainder, LRU cache of 6
+    lengths): calls of 1..51 sweeps, more distinct lengths than the cache
+    holds, some prepared ahead (cmc_engine_prepare), give the same chains
+    bit for bit as one run()."""
+    from ctypes import byref
+    from paper_1606_06659_b200._abi import CmcError
+    counts, X, h = heterosis(2100, seed=3)
+    lengths = [1, 2, 3, 5, 7, 11, 13, 50, 51, 3, 1, 7]
+    total = sum(lengths)
+    cfg = RunConfig(chains=2, burnin=60, iterations=total - 60, thin=4, seed=12, save_genes=6)
+    a = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg, contrasts=[heterosis_contrast()])
+    ref = a.run()
+    b = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg, contrasts=[heterosis_contrast()])
+    lib, hd, err = b._lib, b.handle, CmcError()
+    assert lib.cmc_engine_begin(hd, byref(err)) == 0
+    for n in (13, 51):
+        assert lib.cmc_engine_prepare(hd, n, byref(err)) == 0
+    m = 1
+    for n in lengths:
+        assert lib.cmc_engine_sweeps(hd, m, m + n, byref(err)) == 0, err.msg
+        m += n
+    assert lib.cmc_engine_sync(hd, byref(err)) == 0, err.msg
+    for c in range(2):
+        o = b._output(c)
+        assert np.array_equal(o.final_state.pack(), ref[c].final_state.pack())
+        assert np.array_equal(o.beta_acc.mean, ref[c].beta_acc.mean)
+        assert np.array_equal(o.eps_acc.meansq, ref[c].eps_acc.meansq)
+        assert np.array_equal(o.samples, ref[c].samples)
+        assert np.array_equal(o.contrasts[0].prob, ref[c].contrasts[0].prob)
