@@ -257,7 +257,8 @@ double orc_log_fc_sigma(double sigma, long G, double ss, double s_bound) {
  * q = (beta - theta)^2 / (2 sigma^2) and beta ~ N(theta, sigma^2 xi):
  *   laplace   xi ~ Exp(rate 1/2):        -log(xi)/2 - q/xi - xi/2
  *   t(k)      xi ~ IG(k/2, k/2):         -(k/2 + 3/2) log(xi) - (q + k/2)/xi
- *   horseshoe sqrt(xi) ~ Cauchy+(0,1):   -log(xi) - q/xi - log1p(xi)
+ *   horseshoe sqrt(xi) ~ Cauchy+(0,1):   -log(xi) - q/xi - log1p(xi),
+ *             evaluated as -log(xi (1 + xi)) - q/xi (one log) below 1e150
  * and -inf for xi <= 0. */
 double orc_log_fc_xi(int prior, double xi, double q, double k) {
   if (!(xi > 0.0)) return -INFINITY;
@@ -267,7 +268,7 @@ double orc_log_fc_xi(int prior, double xi, double q, double k) {
     case CMC_PRIOR_T:
       return -(0.5 * k + 1.5) * log(xi) - (q + 0.5 * k) / xi;
     case CMC_PRIOR_HORSESHOE:
-      return -log(xi) - q / xi - log1p(xi);
+      return xi < 1e150 ? -log(xi * (1.0 + xi)) - q / xi : -log(xi) - q / xi - log1p(xi);
     default:
       return 0.0;
   }

@@ -410,7 +410,8 @@ struct BetaF {
 // oracle's orc_log_fc_xi: q = (beta - theta)^2 / (2 sigma^2),
 //   laplace   -log(x)/2 - q/x - x/2
 //   t(k)      -(k/2 + 3/2) log(x) - (q + k/2)/x
-//   horseshoe -log(x) - q/x - log1p(x)
+//   horseshoe -log(x) - q/x - log1p(x), evaluated as -log(x (1 + x)) - q/x
+//             (one log) below 1e150, as the oracle does
 struct XiF {
   int fam;
   double q, k;
@@ -418,7 +419,7 @@ struct XiF {
     if (!(x > 0.0)) return -INFINITY;
     if (fam == CMC_PRIOR_LAPLACE) return -0.5 * log(x) - q / x - 0.5 * x;
     if (fam == CMC_PRIOR_T) return -(0.5 * k + 1.5) * log(x) - (q + 0.5 * k) / x;
-    return -log(x) - q / x - log1p(x);
+    return x < 1e150 ? -log(x * (1.0 + x)) - q / x : -log(x) - q / x - log1p(x);
   }
 };
 

@@ -30,7 +30,12 @@ def test_log_conditionals_closed_forms():
             assert L_.orc_log_fc_xi(T, xi, q, 3.0) == \
                 -(0.5 * 3.0 + 1.5) * math.log(xi) - (q + 0.5 * 3.0) / xi
             assert L_.orc_log_fc_xi(HORSESHOE, xi, q, 0.0) == \
-                -math.log(xi) - q / xi - math.log1p(xi)
+                -math.log(xi * (1.0 + xi)) - q / xi
+            assert abs(L_.orc_log_fc_xi(HORSESHOE, xi, q, 0.0) -
+                       (-math.log(xi) - q / xi - math.log1p(xi))) < 1e-13 * (1 + q / xi)
+    for xi in (1e151, 1e200):   # x (1 + x) would overflow: the two-log form
+        assert L_.orc_log_fc_xi(HORSESHOE, xi, 0.5, 0.0) == \
+            -math.log(xi) - 0.5 / xi - math.log1p(xi)
     for fam in (LAPLACE, T, HORSESHOE):
         assert L_.orc_log_fc_xi(fam, 0.0, 0.7, 3.0) == -math.inf
         assert L_.orc_log_fc_xi(fam, -1.0, 0.7, 3.0) == -math.inf
