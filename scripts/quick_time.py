@@ -7,7 +7,7 @@ from ctypes import byref
 from paper_1606_06659_b200 import _abi, builtin_design, generate, SimSpec, GibbsEngine, ModelSpec, RunConfig, CountMatrix
 from paper_1606_06659_b200._abi import CmcError
 
-def timeit(G, chains, N=16, burn=200, K=100):
+def timeit(G, chains, N=16, burn=200, K=int(os.environ.get("QT_K", "100"))):
     X = builtin_design("heterosis16x5", N)
     counts = generate(SimSpec(G=G, N=N, X=X, nu=8, tau=0.7, theta=[2.5,.2,.2,0,.1], sigma=[.4,.25,.25,.15,.2], seed=1)).counts
     eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, np.zeros(N)), RunConfig(chains=chains, burnin=burn, iterations=K+10, thin=20, seed=7))
@@ -20,6 +20,7 @@ def timeit(G, chains, N=16, burn=200, K=100):
     s = torch.cuda.ExternalStream(lib.cmc_engine_stream(h))
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     assert lib.cmc_engine_sweeps(h, burn + 1, burn + 6, byref(err)) == 0
+    assert lib.cmc_engine_prepare(h, K, byref(err)) == 0
     torch.cuda.synchronize()
     e0.record(s)
     assert lib.cmc_engine_sweeps(h, burn + 6, burn + 6 + K, byref(err)) == 0
