@@ -981,11 +981,13 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_MIN_BLOCKS)
 // The same step for a launch with a horseshoe column (xi_park_kernel).
 // Divergence: a horseshoe xi's slice loop is heavy-tailed (long step-outs,
 // many shrinks), and a warp runs as long as its slowest lane.  So the loop
-// runs at most p.xi_trips trips for every lane (the warp-level vote of
-// __syncthreads_count decides whether any lane is left), then every lane
-// still running parks its whole state (slice state, Philox queue, density
-// parameter) in shared memory, and the block's first threads resume the
-// parked steps densely packed, one per thread.  The continuation draws the
+// runs at most p.xi_trips trips for every lane, then every lane still
+// running parks its whole state (slice state, Philox queue, density
+// parameter) in shared memory -- a warp vote (__ballot_sync) gives each
+// warp its running lanes, the warp's leader reserves that many queue slots
+// with one atomic, and each lane takes its rank among them -- and the
+// block's first threads resume the parked steps densely packed, one per
+// thread.  The continuation draws the
 // same uniforms in the same order, so the result is unchanged.
 struct XiParked {
   SliceRun s;
@@ -1052,8 +1054,13 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_PARK_MIN_BLOCKS)
   }
   // park the lanes still running
   const bool parked = alive && res == kSliceRunning;
+  const unsigned vote = __ballot_sync(0xffffffffu, parked);
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == 0 && vote) base = atomicAdd(&n_park, __popc(vote));
+  base = __shfl_sync(0xffffffffu, base, 0);
   if (parked) {
-    const int k = atomicAdd(&n_park, 1);
+    const int k = base + __popc(vote & ((1u << lane) - 1u));
 #ifdef CMC_DEBUG_BOUNDS
     assert(k >= 0 && k < kXiPark);
 #endif
