@@ -250,17 +250,19 @@ def test_iterate_after_run_leaves_the_run_untouched():
     assert not len(mismatch(p[keep], ost[keep]))
 
 
-def test_step_timing_mode_is_bit_identical_and_reports_every_step():
+@pytest.mark.parametrize("prior", [None, ["normal", "horseshoe", "t", "laplace", "normal"]])
+def test_step_timing_mode_is_bit_identical_and_reports_every_step(prior, tmp_path):
     """The per-step timing mode (reference StepTimings,
     P:src/engine.cpp:173-176): each step launched on its own with events
     between them.  Same results bit for bit; every one of the seven steps
     gets device time (the reference's step order: epsilon, gamma, nu, tau,
     beta, theta, sigma)."""
+    from paper_1606_06659_b200 import PriorConfig
     counts, X, h = heterosis(3000, seed=5)
+    spec = ModelSpec(X, h, PriorConfig(beta_prior=prior, t_df=3.0)) if prior else ModelSpec(X, h)
     cfg = RunConfig(chains=2, burnin=20, iterations=20, thin=5, seed=9, save_genes=5)
-    a = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg,
-                    contrasts=[heterosis_contrast()]).run()
-    eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg, contrasts=[heterosis_contrast()])
+    a = GibbsEngine(CountMatrix(counts), spec, cfg, contrasts=[heterosis_contrast()]).run()
+    eng = GibbsEngine(CountMatrix(counts), spec, cfg, contrasts=[heterosis_contrast()])
     eng.set_step_timing(True)
     b = eng.run()
     for c in range(2):
@@ -272,6 +274,13 @@ def test_step_timing_mode_is_bit_identical_and_reports_every_step():
         assert st.shape == (7,) and np.all(st > 0), st
         # the fused schedule reports one device time under the first step
         assert a[c].step_seconds[0] > 0 and np.all(a[c].step_seconds[1:] == 0)
+    # the results writer's run_report.json carries the seven steps
+    import json
+    eng.write_results(str(tmp_path), wall_seconds=1.0)
+    rep = json.loads((tmp_path / "run_report.json").read_text())
+    steps = rep["step_seconds"]
+    assert set(steps) == {"epsilon", "gamma", "nu", "tau", "beta", "theta", "sigma"}
+    assert all(v > 0 for v in steps.values()), steps
 
 
 def test_sweep_calls_of_any_length_replay_the_same_sweeps():
