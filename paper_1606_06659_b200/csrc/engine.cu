@@ -1804,8 +1804,9 @@ int cmc_engine_launches_per_sweep(const cmc_engine* e) {
 // Per-phase device time of `reps` further monitored sweeps of every chain
 // (one launch per phase for all chains, serialised on the engine stream,
 // CUDA events between phases).  ms[CMC_PHASES]: eps (step 1), gene (steps
-// 2 + 5), xi, leaf_a (+ nu, tau, theta), leaf_b (+ sigma, monitors),
-// gene_contrast; averages per sweep.
+// 2 + 5 and the fused leaf sums), xi, hyper_a (nu, tau, theta; with a xi
+// prior leaf_a), leaf_b (+ sigma, monitors), gene_contrast; averages per
+// sweep.
 int cmc_engine_profile_phases(cmc_engine* e, long m_begin, long reps, double* ms,
                               cmc_error* err) {
   if (!e || reps < 1 || !e->begun || !ms) {

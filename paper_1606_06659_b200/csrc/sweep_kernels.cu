@@ -2,22 +2,22 @@
 // (reference GibbsEngine::iterate, P:src/engine.cpp:161-370, plus the
 // run_chain monitors, P:src/engine.cpp:409-447).
 //
-// Per iteration m (single GPU, three launches captured in a CUDA graph):
-//   gene_sweep  one thread per gene: eps_g1..eps_gN slice steps (step 1),
-//               gamma_g (step 2), beta_g1..beta_gL (step 5), fused Welford
-//               monitors, per-gene contrasts and thinning of saved genes.
-//               Steps 1, 2 and 5 fuse because beta's full conditional does
-//               not read nu, tau or gamma (P:src/engine.cpp:275-331) and
-//               everything else it needs is the previous iteration's
-//               hyperparameters.
-//   leaf_a      one block per 1024-gene reduction leaf: serial leaf sums of
-//               log gamma, 1/gamma, beta_l (the reference tree,
-//               P:include/countmc/parallel.hpp:67-84); the last block to
-//               finish draws nu, tau (steps 3-4) and theta (step 6).
+// Per iteration m and chain lane (single GPU, captured in CUDA graphs):
+//   eps_sweep   one thread per (gene, sample): eps_gn (step 1) and its
+//               Welford monitor.
+//   gene_sweep  one thread per gene: gamma_g (step 2), beta_g1..beta_gL
+//               (step 5), their monitors, per-gene contrasts, thinning; the
+//               last of a 1024-gene leaf's blocks sums the leaf (log gamma,
+//               1/gamma, beta_l: the reference tree's leaves,
+//               P:include/countmc/parallel.hpp:67-84).
+//   hyper_a     one block per chain: pairwise sums over the leaves, nu, tau
+//               (steps 3-4) and theta (step 6).
 //   leaf_b      leaf sums of (beta_l - theta_l)^2; the last block draws
 //               sigma (step 7) and updates the hyper monitors / thinning.
-// Multi-GPU runs the leaf kernels on local leaves, all-gathers the partial
-// sums, and runs hyper_a / hyper_b as separate single-block kernels.
+// With a xi prior the xi kernel follows the gene kernel and leaf_a (its
+// last block running steps 3, 4, 6) replaces the fused leaf sums.
+// Multi-GPU sums local leaves, all-gathers the partial sums (with each
+// rank's stall flag), and runs hyper_a / hyper_b as single-block kernels.
 //
 // Compiled with -fmad=false: every expression below rounds exactly as the
 // reference's non-FMA x86-64 build (P:CMakeLists.txt:7-9), which makes the
