@@ -1276,13 +1276,14 @@ int cmc_engine_create(const cmc_problem* p, const cmc_run_config* config,
   {
     // the gene kernel keeps lp (N) and, beyond 2 groups per column, the
     // group sums (2 Jmax) per gene in shared memory
-    // (1 KB reserved for the kernel's static shared memory; ensure_device
-    // checks the exact total against the device's opt-in limit)
+    // (5 KB reserved for the kernel's static shared memory: the exp table
+    // and the Philox queues' second blocks; ensure_device checks the exact
+    // total against the device's opt-in limit)
     const int smem = gene_sweep_smem_bytes((int)p->N, jmax <= 2 ? 0 : jmax);
-    if (smem + 1024 > 227 * 1024) {
+    if (smem + 5 * 1024 > 227 * 1024) {
       delete e;
       return fail_config(err, "N (plus 2x the groups per model-matrix column) too large for "
-                              "this build's gene kernel: at most 226 samples");
+                              "this build's gene kernel: at most 222 samples");
     }
   }
 

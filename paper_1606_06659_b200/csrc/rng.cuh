@@ -187,6 +187,89 @@ struct Stream {
   }
 };
 
+#ifdef __CUDACC__
+// Stream with the pre-generated second block kept in shared memory instead
+// of registers (4 words per thread at a 32-bit shared-window address, word
+// i at bs + i * stride so a warp's accesses are conflict-free): the same
+// outputs in the same order, 8 fewer live registers.
+struct StreamSm {
+  uint64_t k0, k1, it, site;
+  uint64_t a0, a1, a2, a3;
+  unsigned bs, stride;  // shared-window address of word 0, bytes between words
+  uint32_t block;   // next block index (counter word 2) to generate
+  uint32_t na, nb;  // outputs left in queue a / block b valid (4 or 0)
+
+  __device__ __forceinline__ void st(int i, uint64_t v) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(bs + stride * i), "l"(v));
+  }
+  __device__ __forceinline__ uint64_t ld(int i) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(bs + stride * i));
+    return v;
+  }
+  __device__ __forceinline__ void init(uint64_t seed, uint64_t chain, uint64_t iteration,
+                                       uint64_t site_, unsigned b_smem, unsigned b_stride) {
+    k0 = seed;
+    k1 = chain;
+    it = iteration;
+    site = site_;
+    bs = b_smem;
+    stride = b_stride;
+    block = 0;
+    na = 0;
+    nb = 0;
+  }
+  __device__ __forceinline__ void init_x2(uint64_t seed, uint64_t chain, uint64_t iteration,
+                                          uint64_t site_, unsigned b_smem, unsigned b_stride) {
+    init(seed, chain, iteration, site_, b_smem, b_stride);
+    uint64_t a[4], b[4];
+    philox4x64_10_x2(it, site, 0, k0, k1, a, b);
+    a0 = a[0]; a1 = a[1]; a2 = a[2]; a3 = a[3];
+    st(0, b[0]); st(1, b[1]); st(2, b[2]); st(3, b[3]);
+    block = 2;
+    na = 4;
+    nb = 4;
+  }
+  __device__ __forceinline__ void refill() {
+    if (nb) {
+      a0 = ld(0); a1 = ld(1); a2 = ld(2); a3 = ld(3);
+      nb = 0;
+    } else {
+      uint64_t o[4];
+      philox4x64_10(it, site, block, 0, k0, k1, o);
+      a0 = o[0]; a1 = o[1]; a2 = o[2]; a3 = o[3];
+      ++block;
+    }
+    na = 4;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    if (na == 0) refill();
+    const uint64_t x = a0;
+    a0 = a1;
+    a1 = a2;
+    a2 = a3;
+    --na;
+    return x;
+  }
+  __device__ __forceinline__ double u01() {
+    return ((double)(next() >> 11) + 0.5) * 0x1.0p-53;
+  }
+  __device__ __forceinline__ uint64_t uniform_int_pre(uint64_t n, uint64_t reject_below,
+                                                      uint64_t inv) {
+    for (;;) {
+      const uint64_t x = next();
+      if (x >= reject_below) {
+        uint64_t hi, lo;
+        mulhilo64(x, inv, hi, lo);
+        uint64_t r = x - hi * n;
+        if (r >= n) r -= n;
+        return r;
+      }
+    }
+  }
+};
+#endif
+
 #ifdef __CUDA_ARCH__
 #define CMC_LOG(x) ::log(x)
 #define CMC_SQRT(x) ::sqrt(x)

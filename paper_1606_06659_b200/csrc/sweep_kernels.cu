@@ -67,10 +67,10 @@ __device__ __forceinline__ void tune_update(double& w, double& wa, long m,
 // trip body is branch-free (each lane computes every phase's update and
 // keeps the one its phase selects), so diverged lanes still issue as one
 // SIMT stream; only the rare refill of a third Philox block branches.
-template <class F>
+template <class F, class RNG = Stream>
 __device__ __forceinline__ double slice_step(F& f, double x0, double& w,
                                              double& wa, const SliceCfg& sc,
-                                             long m, Stream& rng,
+                                             long m, RNG& rng,
                                              bool& stalled) {
   const double fx0 = f(x0);
   const double logu = fx0 + log(rng.u01());
@@ -215,10 +215,10 @@ __device__ __forceinline__ int slice_trips(F& f, const SliceCfg& sc, Stream& rng
 // shrinkage phase uses the full density.  F provides operator() (full),
 // side_init(lo, hi, w), any_fresh(), eval_l/eval_r<FRESH>(x, counted) and
 // step_l/step_r().
-template <class F>
+template <class F, class RNG>
 __device__ __forceinline__ double slice_step_so2(F& f, double x0, double& w,
                                                  double& wa, const SliceCfg& sc,
-                                                 long m, Stream& rng,
+                                                 long m, RNG& rng,
                                                  bool& stalled) {
   const double fx0 = f(x0);
   const double logu = fx0 + log(rng.u01());
@@ -610,8 +610,10 @@ __device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
 // blocks (72 registers, no spill) edge out 8 (64 registers, 16-byte
 // spill): 0.3330 vs 0.3338 ms per 4-chain sweep, 0.133 vs 0.136 ms at 1
 // chain (A/B, two reps each).
+// r02: with the Philox queue's second block in shared memory, 8 blocks (64
+// registers, no spill): 0.3261 vs 0.3281 ms per 4-chain sweep (A/B).
 #ifndef CMC_EPS_MIN_BLOCKS
-#define CMC_EPS_MIN_BLOCKS 7
+#define CMC_EPS_MIN_BLOCKS 8
 #endif
 __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
     eps_sweep_kernel(const SweepParams p, const long m_off) {
@@ -660,8 +662,12 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
   const double x0 = p.eps[ie];
   double w = p.eps_w[ie];
   double wa = tuning ? p.eps_wa[ie] : 0.0;
-  Stream rng;
-  rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n));
+  // the Philox queue's second block in shared memory (StreamSm): 64
+  // registers without spills, 8 blocks per SM
+  __shared__ uint64_t rngq[4 * kGeneBlock];
+  StreamSm rng;
+  rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteEps, gg * N + n),
+              (unsigned)__cvta_generic_to_shared(rngq + threadIdx.x), 8u * kGeneBlock);
   bool st = false;
   const double x1 = slice_step_so2(f, x0, w, wa, sc, m, rng, st);
   // The shrink loop's lanes leave at different trips (a return inside the
@@ -704,10 +710,16 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 // normal) is compiled without the xi step.
 // PH: the steps this launch runs, bit 0 step 2 (gamma), bit 1 step 5
 // (beta); the sweep runs both (3), the per-step timing mode one at a time.
+// the gene kernel's Philox queues keep their second block in shared memory
+// (StreamSm: spills 152 -> 100 bytes)
+using GeneRng = StreamSm;
+#define GENE_RNG_Q , rngq_s, 8u * kGeneThreads
 template <int JR, bool XI, int PH>
 __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long m_off,
                                                 double* smem, const ExpTab etab) {
   WarpTrace wt(p, 2, p.slot_base + blockIdx.y);
+  __shared__ uint64_t rngq[4 * kGeneThreads];
+  const unsigned rngq_s = (unsigned)__cvta_generic_to_shared(rngq + threadIdx.x);
   const int tid = threadIdx.x;
   const int slot = p.slot_base + blockIdx.y;
   Hyper* hp = p.hyper + slot;
@@ -765,12 +777,13 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
       const double nu = hp->nu, tau = hp->tau;
       const double shape = (nu + (double)N) / 2.0;
       const double scale = (nu * tau + ss) / 2.0;
-      Stream rng;
       if (p.direct) {
+        Stream rng;
         rng.init(p.seed, chain, (uint64_t)m, site_id(kSiteGamma, gg));
         gnew = 1.0 / gamma_draw(rng, shape, scale);
       } else {
-        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteGamma, gg));
+        GeneRng rng;
+        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteGamma, gg) GENE_RNG_Q);
         InvGammaF f{-(shape + 1.0), scale};
         w0 = p.gam_w[so * G + gl];
         w = w0;
@@ -832,8 +845,8 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
         w0 = beta_w[i];
         w = w0;
         wa = tuning ? beta_wa[i] : 0.0;
-        Stream rng;
-        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l));
+        GeneRng rng;
+        rng.init_x2(p.seed, chain, (uint64_t)m, site_id(kSiteBeta, gg * L + l) GENE_RNG_Q);
         if constexpr (JR > 0) {
           BetaFR<JR> f;
           f.a = __ldg(p.A + i);

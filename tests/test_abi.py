@@ -132,12 +132,20 @@ def test_sample_count_beyond_gene_kernel_shared_memory():
     from paper_1606_06659_b200 import builtin_design
     X = builtin_design("heterosis16x5", 240)
     counts = np.ones((8, 240), np.int64)
-    with pytest.raises(ConfigError, match="at most 226 samples"):
+    with pytest.raises(ConfigError, match="at most 222 samples"):
         GibbsEngine(CountMatrix(counts), ModelSpec(X, np.zeros(240)),
                     RunConfig(chains=1, burnin=10, iterations=10))
-    X = builtin_design("heterosis16x5", 224)   # fits
-    GibbsEngine(CountMatrix(np.ones((8, 224), np.int64)), ModelSpec(X, np.zeros(224)),
-                RunConfig(chains=1, burnin=10, iterations=10))
+    from helpers import two_col_design
+    for N, fits in ((222, True), (223, False)):
+        X = two_col_design(N)
+        make = lambda: GibbsEngine(CountMatrix(np.ones((8, N), np.int64)),  # noqa: E731
+                                   ModelSpec(X, np.zeros(N)),
+                                   RunConfig(chains=1, burnin=10, iterations=10))
+        if fits:
+            make()
+        else:
+            with pytest.raises(ConfigError, match="at most 222 samples"):
+                make()
 
 
 @pytest.mark.parametrize("G,N,seed,nu,tau,theta", [
