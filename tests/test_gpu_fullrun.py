@@ -20,15 +20,20 @@ from helpers import HETEROSIS, Product, heterosis, mismatch
 pytestmark = pytest.mark.gpu
 
 
+LONG = os.environ.get("CMC_LONG") == "1"
+
+
 @pytest.mark.usefixtures("ref")
-def test_default_run_bit_identical_to_reference():
-    counts, X, h = heterosis(1000, seed=99)
+@pytest.mark.parametrize("G", [1000, pytest.param(39656, marks=pytest.mark.skipif(
+    not LONG, reason="Paschold-size whole run: about 5 minutes of reference time; CMC_LONG=1"))])
+def test_default_run_bit_identical_to_reference(G):
+    counts, X, h = heterosis(G, seed=99)
     workers = max(1, min(16, os.cpu_count() or 1))
     cfg = _abi.make_config(chains=4, burnin=2000, iterations=4000, thin=20, seed=3,
                            save_genes=20, workers=workers)
     gpu = Product(counts, X, h, cfg, contrasts=[HETEROSIS]).run()
     ref = oracle.RefEngine(counts, X, h, cfg, contrasts=[HETEROSIS], workers=workers).run()
-    G, N, L = 1000, 16, 5
+    N, L = 16, 5
     th0 = G * N + G + G * L
     for c in range(4):
         a, b = gpu[c], ref[c]
