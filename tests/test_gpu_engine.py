@@ -314,3 +314,24 @@ def test_sweep_calls_of_any_length_replay_the_same_sweeps():
         assert np.array_equal(o.eps_acc.meansq, ref[c].eps_acc.meansq)
         assert np.array_equal(o.samples, ref[c].samples)
         assert np.array_equal(o.contrasts[0].prob, ref[c].contrasts[0].prob)
+
+
+def test_progress_callback_reports_every_chain_and_keeps_results():
+    """set_progress (P:include/countmc/engine.hpp:138-139): run() then
+    enqueues its sweeps in chunks and reports (chain, m, total) after each;
+    the chains are the same bits as a run without a callback."""
+    counts, X, h = heterosis(1500, seed=4)
+    cfg = RunConfig(chains=3, burnin=400, iterations=700, thin=10, seed=6)
+    plain = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg).run()
+    eng = GibbsEngine(CountMatrix(counts), ModelSpec(X, h), cfg)
+    seen = []
+    eng.set_progress(lambda c, m, total: seen.append((c, m, total)))
+    outs = eng.run()
+    total = 1100
+    assert {c for c, _, _ in seen} == {0, 1, 2}
+    for c in range(3):
+        ms = [m for cc, m, t in seen if cc == c]
+        assert ms == sorted(ms) and ms[-1] == total
+        assert all(t == total for cc, _, t in seen if cc == c)
+        assert np.array_equal(outs[c].final_state.pack(), plain[c].final_state.pack())
+        assert np.array_equal(outs[c].beta_acc.mean, plain[c].beta_acc.mean)
