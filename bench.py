@@ -310,6 +310,12 @@ def run_b200(a, rank, world, local_rank):
     # They run in calls of K sweeps, so the K-sweep CUDA graph the timed call
     # replays is captured here, outside the timed region.
     n_probe = max(K, min(n_probe_max, int(400.0 / max(warm_ms, 1e-3)) // K * K))
+    if dist:
+        # every rank must run the same sweeps (each sweep's all-gathers are
+        # collective): rank 0's probe length for all
+        t = torch.tensor([n_probe], device="cuda", dtype=torch.int64)
+        torch.distributed.broadcast(t, 0)
+        n_probe = int(t.item())
     m0 = B + 1 + W + n_probe
     clocks = Clocks(local_rank)
     clocks.start()
