@@ -65,13 +65,16 @@ def parse():
     ap.add_argument("--no-xi", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # test hook: run the sharded (N > 1) code path as a 1-rank NCCL clique
+    # (process group, uid broadcast, shard, collectives, stall exchange)
+    ap.add_argument("--force-shard", action="store_true")
     return ap.parse_args()
 
 
 def workload(a, world):
     key = a.workload
     if key == "auto":
-        key = "paschold" if world == 1 else "g1m"
+        key = "paschold" if world == 1 and not getattr(a, "force_shard", False) else "g1m"
     return (key,) + WORKLOADS[key]
 
 
@@ -230,7 +233,7 @@ def run_b200(a, rank, world, local_rank):
     from paper_1606_06659_b200 import (CountMatrix, GibbsEngine, ModelSpec, RunConfig,
                                        heterosis_contrast)
     from paper_1606_06659_b200._abi import CMC_PHASES, PHASE_NAMES, CmcError
-    dist = world > 1
+    dist = world > 1 or a.force_shard
     torch.cuda.set_device(local_rank)
     key, wname, G, N = workload(a, world)
     counts, X, h = problem(G, N)
@@ -608,10 +611,15 @@ def main():
     if a.impl == "reference":
         run_reference(a, rank, world)
         return
-    if world > 1:
-        # NCCL init logging (nranks per communicator) for the driver's check
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if world > 1 or a.force_shard:
+        # NCCL init logging (nranks per communicator) for the driver's check;
+        # set outright: an inherited NCCL_DEBUG=WARN would hide it
+        # to stderr: stdout carries the one JSON line
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
+        print(f"[bench] rank {rank}: NCCL_DEBUG=INFO NCCL_DEBUG_SUBSYS=INIT (stderr)",
+              file=sys.stderr)
         import torch
         import torch.distributed as td
         torch.cuda.set_device(local_rank)
@@ -619,7 +627,7 @@ def main():
     try:
         run_b200(a, rank, world, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or a.force_shard:
             import torch.distributed as td
             td.destroy_process_group()
 
