@@ -468,6 +468,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.leaves_per_rank = (int)lpr;
   p.world = e->world;
   p.Jmax = e->Jmax;
+  p.beta_carry = beta_carry_ok((int)e->N, e->Jmax);
   p.fuse_tail = e->split_tail ? 0 : 1;
   // without a xi prior the gene kernel sums its own leaves (the xi sums
   // need the xi kernel's draws: leaf_a kernel)

@@ -90,6 +90,7 @@ struct SweepParams {
   int leaves_per_rank;  // leaf stride of the gathered partial buffers
   int world;
   int Jmax;
+  int beta_carry;  // gene kernel carries exp(lp_n) across the beta columns (beta_carry_ok)
   int fuse_tail;  // single GPU: the last leaf block runs the hyper step
   int fuse_leaf_a;  // the gene kernel's last block per leaf sums it (no xi prior)
   unsigned int* leaf_cnt;  // [slots][n_leaves_local] finished gene blocks per leaf
@@ -190,6 +191,13 @@ cudaError_t launch_fastmath_setup(cudaStream_t s);
 cudaError_t launch_compute_A(const double* y, const double* X, double* A,
                              int G, int N, int L, cudaStream_t s);
 int gene_sweep_smem_bytes(int N, int Jmax);
+// The register-group gene kernel (Jmax <= 2) carries exp(lp_n) through the
+// beta columns in a second [N][B] shared array when that keeps it at its
+// resident block count (N <= kBetaCarryMaxN; CMC_BETA_CARRY=0 turns it off).
+constexpr int kBetaCarryMaxN = 16;
+int beta_carry_ok(int N, int Jmax);
+// dynamic shared memory of the gene kernel variant an engine launches
+int gene_dyn_smem(int N, int Jmax);
 // Raise the dynamic shared-memory opt-in of the gene kernel variant for
 // (N, Jmax, xi) on the current device (never lowers it: engines of one
 // process may share a device); *total = its static + dynamic bytes per

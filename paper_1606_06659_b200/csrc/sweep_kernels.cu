@@ -28,6 +28,7 @@
 #include "rng.cuh"
 #include <algorithm>
 #include <cassert>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -746,6 +747,8 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
   double* xs = smem;                             // [N][B]: lp
   double* sS = smem + (size_t)N * kGeneThreads;    // [Jmax][B]
   double* sLogS = sS + (size_t)p.Jmax * kGeneThreads;
+  // JR > 0 with p.beta_carry: xe_n = exp(lp_n) in the group-sum rows
+  double* xe = sS;
   unsigned clamps = 0;
 
   // lp_n = (h_n + eps_n) + xb_n with the new eps and the previous beta,
@@ -766,6 +769,25 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
     const double e = alive ? eps[(size_t)n * G + gl] : 0.0;
     if constexpr (GAM) ss += e * e;
     if constexpr (BET) xs[n * kGeneThreads + tid] = __ldg(p.h + n) + e + xs[n * kGeneThreads + tid];
+  }
+
+  // Carried exps (register-group variant): S_j below is
+  // exp(-v_j bold) * sum_n exp(lp_n), with exp(lp_n) formed once here and
+  // scaled by exp(v_j (bnew - bold)) after each column, instead of one exp
+  // per member and column.  Only the last bits of S_j differ from the
+  // reference's sum of exp(lp_n - v_j bold), and S_j only decides slice
+  // comparisons; every column whose members are not all
+  // inside [-700, 700] (a clamp included) takes the reference's direct sum.
+  bool carry = false;
+  if constexpr (JR > 0 && BET) {
+    if (p.beta_carry && alive) {
+      carry = true;
+      for (int n = 0; n < N; ++n) {
+        const double x = xs[n * kGeneThreads + tid];
+        carry = carry & (x >= -700.0) & (x <= 700.0);
+        xe[n * kGeneThreads + tid] = fast_exp(x, etab);
+      }
+    }
   }
 
   // Step 2: gamma_g, P:src/engine.cpp:204-226 (nu, tau of iteration m-1)
@@ -837,6 +859,21 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
           }
           return s;
         };
+        // the same S_j from the carried exps when every term is in range
+        auto group_sum_c = [&](int j) {
+          const double v = __ldg(p.grp_val + j);
+          const double vb = v * bold;
+          const int q0 = __ldg(p.grp_moff + j), q1 = __ldg(p.grp_moff + j + 1);
+          double s = 0.0;
+          bool ok = (vb > -700.0) & (vb < 700.0);
+          for (int q = q0; q < q1; ++q) {
+            const int n = __ldg(p.grp_mem + q);
+            const double t = xs[n * kGeneThreads + tid] - vb;
+            ok = ok & (t >= -700.0) & (t <= kExpClamp);
+            s += xe[n * kGeneThreads + tid];
+          }
+          return ok ? s * fast_exp(-vb, etab) : group_sum(j);
+        };
         const double sig = hp->sigma[l];
         const double sig2 = sig * sig;
         // prior variance sigma_l^2 (normal) or sigma_l^2 xi_gl (xi column)
@@ -863,7 +900,7 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
             f.lS[jj] = 0.0;
             if (jb + jj < je) {
               f.v[jj] = __ldg(p.grp_val + jb + jj);
-              f.S[jj] = group_sum(jb + jj);
+              f.S[jj] = carry ? group_sum_c(jb + jj) : group_sum(jb + jj);
               f.lS[jj] = log(f.S[jj]);
             }
           }
@@ -893,12 +930,29 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
         beta_w[i] = w;
         beta_wa[i] = wa;
       }
-      if (bnew != bold) {
+      // lp after the last column is not read again (the reference's lp is
+      // scratch, rebuilt at the next sweep's step 5)
+      if (bnew != bold && l + 1 < L) {
         for (int j = jb; j < je; ++j) {
           const double v = __ldg(p.grp_val + j);
+          const double dv = v * (bnew - bold);
+          double f = 1.0;
+          if constexpr (JR > 0) {
+            if (carry) {
+              carry = (dv > -700.0) & (dv < 700.0);
+              f = fast_exp(dv, etab);
+            }
+          }
           for (int q = __ldg(p.grp_moff + j); q < __ldg(p.grp_moff + j + 1); ++q) {
             const int n = __ldg(p.grp_mem + q);
-            xs[n * kGeneThreads + tid] += v * (bnew - bold);
+            const double x = xs[n * kGeneThreads + tid] + dv;
+            xs[n * kGeneThreads + tid] = x;
+            if constexpr (JR > 0) {
+              if (carry) {
+                xe[n * kGeneThreads + tid] *= f;
+                carry = carry & (x >= -700.0) & (x <= 700.0);
+              }
+            }
           }
         }
       }
@@ -1666,6 +1720,20 @@ cudaError_t launch_prio(K kernel, dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kernel, p, m_off);
 }
 
+int beta_carry_ok(int N, int Jmax) {
+  static const int env = [] {
+    const char* v = std::getenv("CMC_BETA_CARRY");  // development override (A/B)
+    return v ? std::atoi(v) : 1;
+  }();
+  return env != 0 && Jmax <= 2 && N <= kBetaCarryMaxN;
+}
+
+int gene_dyn_smem(int N, int Jmax) {
+  if (Jmax > 2) return gene_sweep_smem_bytes(N, Jmax);
+  // the carried exps take the group-sum rows: N + 2 ceil(N/2) >= 2N
+  return gene_sweep_smem_bytes(N, beta_carry_ok(N, Jmax) ? (N + 1) / 2 : 0);
+}
+
 int gene_sweep_smem_bytes(int N, int Jmax) {
   // lp [N][B] and the group sums [2 Jmax][B]; at least kGeneThreads / 32
   // staging rows of kStage for the fused leaf sums
@@ -1711,7 +1779,7 @@ cudaError_t configure_gene_kernels(int N, int Jmax, int xi_any, int* total) {
       cudaSuccess)
     return e;
   const int jr = Jmax <= 2;
-  const int dyn = gene_sweep_smem_bytes(N, jr ? 0 : Jmax);
+  const int dyn = gene_dyn_smem(N, Jmax);
   if (jr) return xi_any ? raise_smem<2, true>(dyn, optin, total) : raise_smem<2, false>(dyn, optin, total);
   return xi_any ? raise_smem<0, true>(dyn, optin, total) : raise_smem<0, false>(dyn, optin, total);
 }
@@ -1719,7 +1787,7 @@ cudaError_t configure_gene_kernels(int N, int Jmax, int xi_any, int* total) {
 template <int JR, bool XI>
 static cudaError_t launch_gene_sweep_t(const SweepParams& p, int chains, long m_off,
                                        cudaStream_t s, int phase) {
-  const int smem = gene_sweep_smem_bytes(p.N, JR > 0 ? 0 : p.Jmax);
+  const int smem = gene_dyn_smem(p.N, p.Jmax);
   dim3 grid((unsigned)((p.G + kGeneThreads - 1) / kGeneThreads), (unsigned)chains);
   if (phase == 1)
     return launch_prio(gene_sweep_kernel<JR, XI, 1>, grid, dim3(kGeneThreads), smem, s,
