@@ -37,11 +37,17 @@ def _case(seed, Gs=(1, 3, 31, 127, 128, 129, 700, 1023, 1024, 1025, 2500)):
     nu, tau, sigma = float(rng.uniform(2, 12)), float(rng.uniform(0.2, 2)), rng.uniform(0.1, 0.6, L)
     for shrink in (1.0, 0.5, 0.25, 0.1):
         # wide continuous designs can overflow the simulator's Poisson mean;
-        # such a case is redrawn at a smaller effect scale
+        # such a case is redrawn at a smaller effect scale.  So is one with
+        # a count above 1e8: at y ~ 1e13 (seed 602 drew 1.2e13) a log
+        # density y*eps - exp(lp) ~ 6e13 is resolved only to its ulp (0.008),
+        # and a last-bit libm difference (exp, log: DESIGN.md section 2) decides
+        # slice comparisons; bit-parity is a claim about the counts RNA-seq has
         try:
             counts = generate(SimSpec(G=G, N=N, X=X, h=h, nu=nu, tau=tau * shrink,
                                       theta=list(theta * shrink), sigma=list(sigma * shrink),
                                       seed=seed)).counts
+            if counts.max() > 1e8 and shrink > 0.1:
+                continue
             break
         except ConfigError:
             continue
