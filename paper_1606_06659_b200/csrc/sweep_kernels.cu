@@ -613,8 +613,11 @@ __device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
 // chain (A/B, two reps each).
 // r02: with the Philox queue's second block in shared memory, 8 blocks (64
 // registers, no spill): 0.3261 vs 0.3281 ms per 4-chain sweep (A/B).
+// r02, after the carried beta exps: 9 blocks (56 registers) with the gene
+// kernel at 5: 0.3268 vs 0.3290 ms (100-sweep calls), 0.3316 vs 0.3330
+// (20-sweep calls), two reps on two boxes; 10 blocks: 0.3289 at 4 chains.
 #ifndef CMC_EPS_MIN_BLOCKS
-#define CMC_EPS_MIN_BLOCKS 8
+#define CMC_EPS_MIN_BLOCKS 9
 #endif
 __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
     eps_sweep_kernel(const SweepParams p, const long m_off) {
@@ -700,10 +703,11 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
 // beta_g1..beta_gL in column order.  Lanes of a warp are re-converged with
 // __syncwarp() at every slice-step boundary so each step's log-density
 // evaluations run as one SIMT stream (no early exits: a lane without a
-// gene, or whose gene stalled, idles with alive == false).  6 blocks per
-// SM (80 registers, small spills) measured best with the eps kernel at 8.
+// gene, or whose gene stalled, idles with alive == false).  5 blocks per
+// SM (96 registers) with the eps kernel at 9 (above); 6 blocks (80
+// registers, 100-byte spills) was best before the carried beta exps.
 #ifndef CMC_GENE_MIN_BLOCKS
-#define CMC_GENE_MIN_BLOCKS 6
+#define CMC_GENE_MIN_BLOCKS 5
 #endif
 // JR > 0: every column has at most JR groups, kept in registers
 // (BetaFR); JR = 0: any design, group sums in shared memory (BetaF).
