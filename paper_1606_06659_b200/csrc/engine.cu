@@ -161,13 +161,22 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  // From the device's default memory pool (cmc_engine_destroy synchronises
+  // the device before any free).  The pool keeps freed memory for the next
+  // engine (set_pool_retention), so an engine created after another one of
+  // similar size maps no new pages: cudaMalloc of a Paschold-size engine's
+  // state took 17-67 ms per create.  The allocation is ordered on this
+  // thread's default stream and synchronised here, so every stream may use
+  // the buffer at once.
   cudaError_t alloc(size_t count) {
     n = count;
     if (count == 0) return cudaSuccess;
-    return cudaMalloc(&p, sizeof(T) * count);
+    cudaError_t r = cudaMallocAsync((void**)&p, sizeof(T) * count, cudaStreamPerThread);
+    if (r != cudaSuccess) return r;
+    return cudaStreamSynchronize(cudaStreamPerThread);
   }
   void free_() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, cudaStreamPerThread);
     p = nullptr;
     n = 0;
   }
@@ -319,9 +328,37 @@ int fail_config(cmc_error* err, const std::string& msg) {
 long prob_len(const cmc_engine* e) { return e->has_ctab ? e->ctab.n_prob : 0; }
 
 // Allocate and upload this shard's problem and all chain state.
+static double tnow() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+// The device's default pool keeps up to this many freed bytes instead of
+// returning them to the driver at the next synchronisation (once per
+// device, never lowered; CMC_POOL_RETAIN_MB overrides, 0 = driver default).
+cudaError_t set_pool_retention(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return cudaSuccess;
+  done.push_back(device);
+  const char* v = std::getenv("CMC_POOL_RETAIN_MB");
+  const unsigned long long mb = v ? std::strtoull(v, nullptr, 10) : 16384ull;
+  if (mb == 0) return cudaSuccess;
+  cudaMemPool_t pool;
+  cudaError_t r = cudaDeviceGetDefaultMemPool(&pool, device);
+  if (r != cudaSuccess) return r;
+  unsigned long long cur = 0;
+  r = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
+  if (r != cudaSuccess) return r;
+  unsigned long long want = mb << 20;
+  if (cur >= want) return cudaSuccess;
+  return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
+}
+
 int ensure_device(cmc_engine* e, cmc_error* err) {
   if (e->dev_ready) return CMC_OK;
+  const double Q0 = tnow();
   CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(set_pool_retention(e->device));
   CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&e->tail_stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&e->ev_gene, cudaEventDisableTiming));
@@ -365,6 +402,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
     }
   }
   // SoA y[n][g] as double (exact for counts < 2^53)
+  const double Q1 = tnow();
   std::vector<double> yh((size_t)N * G);
   for (long g = 0; g < G; ++g)
     for (long n = 0; n < N; ++n)
@@ -408,6 +446,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   // scratch (the reference's iterate works on caller-owned state, so it must
   // not disturb a run).  Accumulators exist for run chains only: iterate()
   // sweeps with the monitors off.
+  const double Q2 = tnow();
   const long Cs = C + 1;
   const size_t gn = (size_t)G * N * C, gl = (size_t)G * L * C, gc = (size_t)G * C;
   const size_t sn = (size_t)G * N * Cs, sl = (size_t)G * L * Cs, sc = (size_t)G * Cs;
@@ -456,6 +495,9 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   CUDA_TRY(cudaMemcpy(e->d_m.p, &one, sizeof(long), cudaMemcpyHostToDevice));
   e->host_m = 1;
 
+  if (std::getenv("CMC_PHASE_LOG"))
+    fprintf(stderr, "ensure: streams %.1f ms, inputs %.1f ms, state allocs %.1f ms\n",
+            1e3 * (Q1 - Q0), 1e3 * (Q2 - Q1), 1e3 * (tnow() - Q2));
   SweepParams& p = e->base;
   std::memset(&p, 0, sizeof(p));
   p.G = (int)G;
@@ -1376,7 +1418,9 @@ int cmc_engine_destroy(cmc_engine* e) {
   if (!e) return CMC_OK;
   if (e->dev_ready) {
     cudaSetDevice(e->device);
-    cudaStreamSynchronize(e->stream);
+    // every lane's work done before the pooled buffers go back (cudaFree
+    // used to imply this)
+    cudaDeviceSynchronize();
     for (auto& g : e->graph)
       if (g) cudaGraphExecDestroy(g);
     DevBuf<double>* ds[] = {&e->y, &e->A, &e->Xd, &e->hd, &e->gval, &e->eps,
@@ -1384,7 +1428,8 @@ int cmc_engine_destroy(cmc_engine* e) {
                             &e->gam_wa, &e->beta, &e->beta_w, &e->beta_wa,
                             &e->log_gam, &e->inv_gam, &e->acc_eps, &e->acc_gam,
                             &e->acc_beta, &e->cprob, &e->samples, &e->partA,
-                            &e->partB, &e->xi, &e->xi_w, &e->xi_wa, &e->acc_xi};
+                            &e->partB, &e->xi, &e->xi_w, &e->xi_wa, &e->acc_xi,
+                            &e->xfer};
     for (auto* b : ds) b->free_();
     e->goff.free_();
     e->gmoff.free_();
@@ -1531,20 +1576,44 @@ int cmc_engine_iterate(cmc_engine* e, long chain, long m, uint64_t* clamps,
 
 int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
   if (!e) return CMC_ERR_ARG;
-  int rc = ensure_device(e, err);
-  if (rc) return rc;
-  CUDA_TRY(cudaSetDevice(e->device));
-  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  const double T0 = tnow();
   const long XI = e->xi_any ? e->G_total * e->L : 0;
   const long S = e->G_total * e->N + e->G_total + e->G_total * e->L + 2 * e->L + 2 + XI;
-  const long T = e->G_total * e->N + e->G_total + e->G_total * e->L + e->L + 2 + XI;
-  (void)T;
-  std::vector<double> st((size_t)S);
+  // The chains' initial states (host, glibc: bit-identical to the
+  // reference) are computed on host threads, one per chain, while this
+  // thread sets up the device (allocations, inputs); up to 2 GB of host
+  // staging, else one chain at a time below.
+  const bool overlap = (double)e->C * (double)S * 8.0 <= 2e9;
+  std::vector<std::vector<double>> sts(overlap ? (size_t)e->C : 0);
+  std::thread init_th;
+  if (overlap)
+    init_th = std::thread([e, S, &sts] {
+      std::vector<std::thread> per;
+      for (long c = 0; c < e->C; ++c)
+        per.emplace_back([e, S, &sts, c] {
+          sts[(size_t)c].resize((size_t)S);
+          initial_state_host(e, c, sts[(size_t)c].data());
+        });
+      for (auto& t : per) t.join();
+    });
+  int rc = ensure_device(e, err);
+  if (init_th.joinable()) init_th.join();
+  if (rc) return rc;
+  const double T1 = tnow();
+  double Tis = 0, Tup = 0;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaStreamSynchronize(e->stream));
+  std::vector<double> st(overlap ? 0 : (size_t)S);
   CUDA_TRY(cudaMemset(e->hyper.p, 0, sizeof(Hyper) * e->C));
   for (long c = 0; c < e->C; ++c) {
-    initial_state_host(e, c, st.data());
-    if ((rc = upload_state(e, c, st.data(), nullptr, nullptr, err))) return rc;
+    double a = tnow();
+    double* sc = overlap ? sts[(size_t)c].data() : st.data();
+    if (!overlap) initial_state_host(e, c, sc);
+    double b = tnow();
+    if ((rc = upload_state(e, c, sc, nullptr, nullptr, err))) return rc;
+    Tis += b - a; Tup += tnow() - b;
   }
+  const double T2 = tnow();
   // fresh tuning of every run chain (TuningState(G, N, L, w_init),
   // P:include/countmc/engine.hpp:58-74): widths w_init, accumulators 0,
   // filled on the device instead of uploading two packed host arrays
@@ -1587,6 +1656,9 @@ int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
   e->step_sec.assign((size_t)e->C * 7, 0.0);
   CUDA_TRY(cudaMemset(e->step_cyc.p, 0, sizeof(unsigned long long) * e->step_cyc.n));
   e->begun = true;
+  if (std::getenv("CMC_PHASE_LOG"))
+    fprintf(stderr, "begin: ensure_device %.1f ms, init states %.1f ms, upload %.1f ms, rest %.1f ms\n",
+            1e3 * (T1 - T0), 1e3 * Tis, 1e3 * Tup, 1e3 * (tnow() - T2));
   return CMC_OK;
 }
 

@@ -543,6 +543,7 @@ class GibbsEngine:
             _raise(self._lib.cmc_engine_begin(self._h, byref(err)), err)
             total = self._cfg.burnin + self._cfg.iterations
             step = max(1, min(total, 500)) if self._progress else total
+            bufs = None
             m = 1
             while m <= total:
                 m_end = min(total + 1, m + step)
@@ -552,8 +553,15 @@ class GibbsEngine:
                     for c in range(self._cfg.chains):
                         self._progress(c, m_end - 1, total)
                 m = m_end
+                if bufs is None:
+                    # the sweeps are enqueued and the host is idle until sync:
+                    # allocate the output arrays now, every page written, so
+                    # the copies after sync do not page-fault (fresh arrays
+                    # of a Paschold-size run cost ~36 ms of faults, 4 chains)
+                    bufs = [self._output_arrays() for _ in range(self._cfg.chains)]
             _raise(self._lib.cmc_engine_sync(self._h, byref(err)), err)
-            self._outputs = [self._output(c) for c in range(self._cfg.chains)]
+            self._outputs = [self._output(c, bufs[c] if bufs else None)
+                             for c in range(self._cfg.chains)]
         return self._outputs
 
     def diagnostics(self) -> Diagnostics:
@@ -659,10 +667,16 @@ class GibbsEngine:
             _raise(self._lib.cmc_engine_set_output(self._h, c, byref(view), byref(err)), err)
         self._outputs = list(outputs)
 
-    def _output(self, chain: int) -> ChainOutput:
+    def _output_arrays(self):
+        """The large per-chain output arrays (4 accumulator blocks and the
+        final state), allocated with every page touched."""
+        S, _, A = sizes(self.G, self.N, self.L, self.xi)
+        return [np.full(A, 0.0) for _ in range(4)], np.full(S, 0.0)
+
+    def _output(self, chain: int, arrays=None) -> ChainOutput:
         G, N, L = self.G, self.N, self.L
         S, _, A = sizes(G, N, L, self.xi)
-        accs = [np.zeros(A) for _ in range(4)]
+        accs, final = arrays if arrays is not None else self._output_arrays()
         count = np.zeros(1, dtype=np.int64)
         n_prob = sum(G if c.per_gene else 1 for c in self._contrast_specs)
         prob = np.zeros(max(1, n_prob))
@@ -671,7 +685,6 @@ class GibbsEngine:
         samples = np.zeros(max(1, self.n_cols * rows))
         iters = np.zeros(max(1, rows), dtype=np.int64)
         clamps = np.zeros(1, dtype=np.uint64)
-        final = np.zeros(S)
         secs = np.zeros(7)
         view = CmcOutputView(lptr(count), dptr(accs[0]), dptr(accs[1]), dptr(accs[2]),
                              dptr(accs[3]), dptr(prob), lptr(ccount), dptr(samples),
