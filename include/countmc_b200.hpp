@@ -307,9 +307,12 @@ class GibbsEngine {
         for (long c = 0; c < cfg_.chains; ++c) progress_(c, m_end - 1, total);
       }
     }
-    check(cmc_engine_sync(h_, &e), e);
+    // the sweeps are enqueued: size (and so page in) the outputs while the
+    // device runs, then copy into them after the sync
     std::vector<ChainOutput> outs;
-    for (long c = 0; c < cfg_.chains; ++c) outs.push_back(output(c));
+    for (long c = 0; c < cfg_.chains; ++c) outs.push_back(alloc_output(c));
+    check(cmc_engine_sync(h_, &e), e);
+    for (auto& o : outs) fill_output(o);
     return outs;
   }
 
@@ -321,7 +324,7 @@ class GibbsEngine {
   long S() const { return G_ * N_ + G_ + G_ * L_ + 2 * L_ + 2 + XI(); }
   long A() const { return 2 + 2 * L_ + G_ * L_ + G_ + G_ * N_ + XI(); }
 
-  ChainOutput output(long chain) {
+  ChainOutput alloc_output(long chain) {
     ChainOutput o;
     o.chain = chain;
     o.mean.resize(A());
@@ -332,6 +335,10 @@ class GibbsEngine {
     o.sample_iters.resize(nrows_);
     o.saved_genes = saved_;
     o.final_state = ChainState{G_, N_, L_, std::vector<double>(S())};
+    return o;
+  }
+
+  void fill_output(ChainOutput& o) {
     cmc_output_view v{};
     v.acc_count = &o.count;
     v.acc_mean = o.mean.data();
@@ -343,8 +350,7 @@ class GibbsEngine {
     v.clamp_events = &o.clamp_events;
     v.final_state = o.final_state.packed.data();
     cmc_error e{};
-    check(cmc_engine_get_output(h_, chain, &v, &e), e);
-    return o;
+    check(cmc_engine_get_output(h_, o.chain, &v, &e), e);
   }
 
   cmc_engine* h_ = nullptr;
