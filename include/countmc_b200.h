@@ -171,6 +171,11 @@ const char* cmc_version(void);
 int cmc_engine_create(const cmc_problem* problem, const cmc_run_config* config,
                       const cmc_contrast_set* contrasts, int device,
                       cmc_engine** out, cmc_error* err);
+/* Device buffers come from the device's default memory pool
+ * (cudaMallocAsync); on first use of a device the library raises that
+ * pool's release threshold to 16 GB (CMC_POOL_RETAIN_MB, 0 = leave the
+ * driver default) so later engines reuse freed memory.  Destroy
+ * synchronises the device before returning the buffers. */
 int cmc_engine_destroy(cmc_engine* engine);
 
 /* Sizes: G, N, L, chains, number of saved genes, thinned columns, rows. */
