@@ -964,7 +964,7 @@ int orc_iterate(const orc_engine* e, double* st, double* tw, double* ta,
   double* xi = e->xi_any ? st + ST_XI(e) : NULL;
   double* xb = (double*)malloc(sizeof(double) * (size_t)(G * N));
   double* lp = (double*)malloc(sizeof(double) * (size_t)(G * N));
-  double* tmp = (double*)malloc(sizeof(double) * (size_t)G);
+  double* tmp = (double*)calloc((size_t)G, sizeof(double));
   int rc = CMC_OK;
   int stalled = 0;
 
