@@ -784,6 +784,13 @@ __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long
   // inside [-700, 700] (a clamp included) takes the reference's direct sum.
   bool carry = false;
   if constexpr (JR > 0 && BET) {
+#ifdef CMC_DEBUG_BOUNDS
+    if (p.beta_carry) {  // lp and the carried exps: 2N rows of dynamic shared memory
+      unsigned dyn;
+      asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+      assert((size_t)2 * N * kGeneThreads * sizeof(double) <= dyn);
+    }
+#endif
     if (p.beta_carry && alive) {
       carry = true;
       for (int n = 0; n < N; ++n) {
