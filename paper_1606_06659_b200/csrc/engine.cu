@@ -511,6 +511,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.world = e->world;
   p.Jmax = e->Jmax;
   p.beta_carry = beta_carry_ok((int)e->N, e->Jmax);
+  p.eps_solo = e->n_lanes == 1 ? 1 : 0;
   p.fuse_tail = e->split_tail ? 0 : 1;
   // without a xi prior the gene kernel sums its own leaves (the xi sums
   // need the xi kernel's draws: leaf_a kernel)

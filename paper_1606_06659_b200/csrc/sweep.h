@@ -90,6 +90,7 @@ struct SweepParams {
   int leaves_per_rank;  // leaf stride of the gathered partial buffers
   int world;
   int Jmax;
+  int eps_solo;    // one chain lane: the eps kernel variant tuned to run alone
   int beta_carry;  // gene kernel carries exp(lp_n) across the beta columns (beta_carry_ok)
   int fuse_tail;  // single GPU: the last leaf block runs the hyper step
   int fuse_leaf_a;  // the gene kernel's last block per leaf sums it (no xi prior)

@@ -616,10 +616,17 @@ __device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
 // r02, after the carried beta exps: 9 blocks (56 registers) with the gene
 // kernel at 5: 0.3268 vs 0.3290 ms (100-sweep calls), 0.3316 vs 0.3330
 // (20-sweep calls), two reps on two boxes; 10 blocks: 0.3289 at 4 chains.
+// A single chain lane (one chain: nothing runs beside the eps kernel)
+// prefers 10 blocks (48 registers): 0.1351 vs 0.1429 ms per 1-chain sweep;
+// with two lanes 10 blocks gave 0.3289 vs 0.3268 ms at 4 chains.
 #ifndef CMC_EPS_MIN_BLOCKS
 #define CMC_EPS_MIN_BLOCKS 9
 #endif
-__global__ void __launch_bounds__(kGeneBlock, CMC_EPS_MIN_BLOCKS)
+#ifndef CMC_EPS_SOLO_MIN_BLOCKS
+#define CMC_EPS_SOLO_MIN_BLOCKS 10
+#endif
+template <int MINB>
+__global__ void __launch_bounds__(kGeneBlock, MINB)
     eps_sweep_kernel(const SweepParams p, const long m_off) {
   __shared__ double exp_tab[32];
   exp_table_init(exp_tab);
@@ -1756,7 +1763,11 @@ int gene_sweep_smem_bytes(int N, int Jmax) {
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
                              cudaStream_t s) {
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)p.N, (unsigned)chains);
-  return launch_prio(eps_sweep_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_eps, p, m_off);
+  if (p.eps_solo)
+    return launch_prio(eps_sweep_kernel<CMC_EPS_SOLO_MIN_BLOCKS>, grid, dim3(kGeneBlock), 0, s,
+                       p.prio_eps, p, m_off);
+  return launch_prio(eps_sweep_kernel<CMC_EPS_MIN_BLOCKS>, grid, dim3(kGeneBlock), 0, s,
+                     p.prio_eps, p, m_off);
 }
 
 template <int JR, bool XI>
