@@ -625,6 +625,12 @@ __device__ void contrast_update(const ContrastTable* t, int ci, double* prob,
 #ifndef CMC_EPS_SOLO_MIN_BLOCKS
 #define CMC_EPS_SOLO_MIN_BLOCKS 10
 #endif
+// with a xi prior (the xi kernel runs after each gene kernel) the eps
+// kernel at 8 and the gene kernel at 6 (below): horseshoe 0.786 -> 0.770,
+// t 0.542 -> 0.535 ms per 4-chain sweep against the normal model's 9 / 5
+#ifndef CMC_EPS_XI_MIN_BLOCKS
+#define CMC_EPS_XI_MIN_BLOCKS 8
+#endif
 template <int MINB>
 __global__ void __launch_bounds__(kGeneBlock, MINB)
     eps_sweep_kernel(const SweepParams p, const long m_off) {
@@ -713,6 +719,9 @@ __global__ void __launch_bounds__(kGeneBlock, MINB)
 // gene, or whose gene stalled, idles with alive == false).  5 blocks per
 // SM (96 registers) with the eps kernel at 9 (above); 6 blocks (80
 // registers, 100-byte spills) was best before the carried beta exps.
+#ifndef CMC_GENE_XI_MIN_BLOCKS
+#define CMC_GENE_XI_MIN_BLOCKS 6  // with a xi prior (see CMC_EPS_XI_MIN_BLOCKS)
+#endif
 #ifndef CMC_GENE_MIN_BLOCKS
 #define CMC_GENE_MIN_BLOCKS 5
 #endif
@@ -1379,7 +1388,7 @@ __device__ void gene_leaf_epilogue(const SweepParams& p, int slot, long m, doubl
 }
 
 template <int JR, bool XI, int PH>
-__global__ void __launch_bounds__(kGeneThreads, CMC_GENE_MIN_BLOCKS)
+__global__ void __launch_bounds__(kGeneThreads, XI ? CMC_GENE_XI_MIN_BLOCKS : CMC_GENE_MIN_BLOCKS)
     gene_sweep_kernel(const SweepParams p, const long m_off) {
   extern __shared__ double smem[];
   __shared__ double exp_tab[32];
@@ -1763,6 +1772,9 @@ int gene_sweep_smem_bytes(int N, int Jmax) {
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,
                              cudaStream_t s) {
   dim3 grid((unsigned)((p.G + kGeneBlock - 1) / kGeneBlock), (unsigned)p.N, (unsigned)chains);
+  if (p.xi_any)
+    return launch_prio(eps_sweep_kernel<CMC_EPS_XI_MIN_BLOCKS>, grid, dim3(kGeneBlock), 0, s,
+                       p.prio_eps, p, m_off);
   if (p.eps_solo)
     return launch_prio(eps_sweep_kernel<CMC_EPS_SOLO_MIN_BLOCKS>, grid, dim3(kGeneBlock), 0, s,
                        p.prio_eps, p, m_off);
