@@ -576,7 +576,11 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
   p.xi_any = e->xi_any ? 1 : 0;
   {
     const char* v = std::getenv("CMC_XI_TRIPS");  // development override (A/B)
-    p.xi_trips = v ? std::atoi(v) : 8;  // A/B: 8 0.749, 16 0.756, 32 0.787, no parking 0.830 ms
+    // horseshoe A/B, ms per 4-chain sweep on the final build (two reps):
+    // 8 0.767, 10 0.746, 12 0.729, 14 0.732, 16 0.739, 20 0.750, 24 0.760
+    // (before the per-model block counts: 8 0.749, 16 0.756, 32 0.787, no
+    // parking 0.830)
+    p.xi_trips = v ? std::atoi(v) : 12;
   }
   for (long l = 0; l < L; ++l) p.xi_fam[l] = e->prior[(size_t)l];
   p.t_df = e->t_df;
