@@ -1903,6 +1903,11 @@ cudaError_t launch_xi_sweep(const SweepParams& p, int chains, long m_off,
   // t 0.523 -> 0.548 with it
   bool hs = false;
   for (int l = 0; l < p.L; ++l) hs |= p.xi_fam[l] == CMC_PRIOR_HORSESHOE;
+  static const int force = [] {  // development override (A/B): 1 park always, 0 never
+    const char* v = std::getenv("CMC_XI_PARK");
+    return v ? std::atoi(v) : -1;
+  }();
+  if (force >= 0) hs = force != 0;
   if (hs) return launch_prio(xi_park_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_gene, p, m_off);
   return launch_prio(xi_sweep_kernel, grid, dim3(kGeneBlock), 0, s, p.prio_gene, p, m_off);
 }
