@@ -46,7 +46,7 @@ def _case(seed, Gs=(1, 3, 31, 127, 128, 129, 700, 1023, 1024, 1025, 2500)):
             counts = generate(SimSpec(G=G, N=N, X=X, h=h, nu=nu, tau=tau * shrink,
                                       theta=list(theta * shrink), sigma=list(sigma * shrink),
                                       seed=seed)).counts
-            if counts.max() > 1e8 and shrink > 0.1:
+            if counts.max() > 1e8:  # seeds 602 and 1271 drew 1.2e13 and 3.3e12
                 continue
             break
         except ConfigError:
