@@ -327,7 +327,7 @@ int fail_config(cmc_error* err, const std::string& msg) {
 
 long prob_len(const cmc_engine* e) { return e->has_ctab ? e->ctab.n_prob : 0; }
 
-// Allocate and upload this shard's problem and all chain state.
+// host wall clock for the CMC_PHASE_LOG set-up split (development aid)
 static double tnow() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -354,6 +354,7 @@ cudaError_t set_pool_retention(int device) {
   return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
 }
 
+// Allocate and upload this shard's problem and all chain state.
 int ensure_device(cmc_engine* e, cmc_error* err) {
   if (e->dev_ready) return CMC_OK;
   const double Q0 = tnow();
