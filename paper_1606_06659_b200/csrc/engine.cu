@@ -184,6 +184,9 @@ struct DevBuf {
 
 }  // namespace
 
+#ifndef CMC_GRAPH_CHUNK
+#define CMC_GRAPH_CHUNK 50  // sweeps per CUDA graph (A/B: 25 0.3551 ms, 50 0.3531, 100 0.3527)
+#endif
 #ifndef CMC_MAX_LANES
 #define CMC_MAX_LANES 2  // chain lanes (r02 A/B with graph upload: 4 lanes 0.3235 vs 0.3273 ms per monitored sweep, but a whole default run() 2.03 vs 1.99 s of sweeps)
 #endif
@@ -1603,6 +1606,26 @@ int cmc_engine_begin(cmc_engine* e, cmc_error* err) {
       for (auto& t : per) t.join();
     });
   int rc = ensure_device(e, err);
+  if (rc == CMC_OK && overlap && !e->loop && !e->split_tail && !e->step_timing) {
+    // the run's sweep graphs (the 50-sweep chunk and the remainder of
+    // burnin + iterations) are captured now, while the initial states are
+    // computed on the other thread, instead of at the first sweeps call
+    // with the device idle (17 ms at G = 39,656, 4 chains)
+    SweepParams p = e->base;
+    p.slot_base = 0;
+    p.chain_base = 0;
+    p.monitor_enabled = 1;
+    const long total = e->cfg.burnin + e->cfg.iterations;
+    cudaGraphExec_t g = nullptr;
+    cudaError_t ce = cudaSuccess;
+    if (total >= CMC_GRAPH_CHUNK) ce = sweep_graph(e, p, CMC_GRAPH_CHUNK, &g);
+    if (ce == cudaSuccess && total % CMC_GRAPH_CHUNK)
+      ce = sweep_graph(e, p, total % CMC_GRAPH_CHUNK, &g);
+    if (ce != cudaSuccess) {
+      set_err(err, CMC_ERR_CUDA, std::string("sweep graph capture: ") + cudaGetErrorString(ce));
+      rc = CMC_ERR_CUDA;
+    }
+  }
   if (init_th.joinable()) init_th.join();
   if (rc) return rc;
   const double T1 = tnow();
@@ -1770,9 +1793,6 @@ int cmc_engine_sweeps(cmc_engine* e, long m_begin, long m_end, cmc_error* err) {
   p.chain_base = 0;
   p.monitor_enabled = 1;
   const long total = m_end - m_begin;
-#ifndef CMC_GRAPH_CHUNK
-#define CMC_GRAPH_CHUNK 50  // sweeps per CUDA graph (A/B: 25 0.3551 ms, 50 0.3531, 100 0.3527)
-#endif
   if (e->step_timing) {
     const int rc = step_timed_sweeps(e, p, total, err);
     if (rc == CMC_OK) e->host_m = m_end;
