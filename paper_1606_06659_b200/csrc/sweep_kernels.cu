@@ -1333,6 +1333,73 @@ __device__ void leaf_a_sums(const SweepParams& p, int slot, long lb, double* sta
   }
 }
 
+// leaf_a_sums for the gene kernel's epilogue (no xi prior): the warps take
+// the quantities in pairs (q, q + nwarps), lane 0 adding the first and lane
+// 1 the second in the same instruction stream, so the 2 + L serial chains
+// of 1,024 additions run in one round of two interleaved chains per warp
+// instead of two rounds of one.  Each chain is still serial in gene order.
+#ifndef CMC_LEAF_PAIRED
+#define CMC_LEAF_PAIRED 1
+#endif
+__device__ void leaf_a_sums_paired(const SweepParams& p, int slot, long lb, double* stage) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int L = p.L, Q = 2 + L, Qs = leaf_qs_a(L, 0);
+  const size_t G = (size_t)p.G, so = (size_t)slot;
+  const long start = lb * kLeaf;
+  const long end = min((long)G, start + kLeaf);
+  const long lpr = p.leaves_per_rank;
+  const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
+  double* bufA = stage + (size_t)warp * 2 * kStage;
+  double* bufB = bufA + kStage;
+  auto src_of = [&](int q) -> const double* {
+    return q < 2 ? (q == 0 ? p.log_gam : p.inv_gam) + so * G
+                 : p.beta + so * L * G + (size_t)(q - 2) * G;
+  };
+  constexpr int PER = kStage / 32;
+  const int chunks = (int)((end - start + kStage - 1) / kStage);
+  for (int qa = warp; qa < Q; qa += 2 * nwarps) {
+    const int qb = qa + nwarps;
+    const double* A = src_of(qa);
+    const double* B = qb < Q ? src_of(qb) : A;
+    double va[PER], vb[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const long idx = start + k * 32 + lane;
+      va[k] = idx < end ? __ldcg(A + idx) : 0.0;
+      vb[k] = idx < end ? __ldcg(B + idx) : 0.0;
+    }
+    double s = 0.0;
+    const double* mine = lane == 1 ? bufB : bufA;
+    for (int c = 0; c < chunks; ++c) {
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        bufA[k * 32 + lane] = va[k];
+        bufB[k * 32 + lane] = vb[k];
+      }
+      __syncwarp();
+      if (c + 1 < chunks) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const long idx = start + (long)(c + 1) * kStage + k * 32 + lane;
+          va[k] = idx < end ? __ldcg(A + idx) : 0.0;
+          vb[k] = idx < end ? __ldcg(B + idx) : 0.0;
+        }
+      }
+      if (lane < 2) {
+#pragma unroll 16
+        for (int i = 0; i < kStage; ++i) s += mine[i];
+      }
+      __syncwarp();
+    }
+#ifdef CMC_DEBUG_BOUNDS
+    assert(rank >= 0 && rank < p.world && slot - p.slot_base < p.C && qa < Qs && lb < lpr);
+#endif
+    double* dst = p.partA + (rank * p.C + (slot - p.slot_base)) * Qs * lpr + lb;
+    if (lane == 0) dst[(size_t)qa * lpr] = s;
+    if (lane == 1 && qb < Q) dst[(size_t)qb * lpr] = s;
+  }
+}
+
 // This rank's stall flag of a chain in the gathered partA section (sharded
 // runs): leaf slot 0 of quantity Q.
 __device__ __forceinline__ void write_stall_flag(const SweepParams& p, int slot, bool st) {
@@ -1373,7 +1440,10 @@ __device__ void gene_leaf_epilogue(const SweepParams& p, int slot, long m, doubl
   __syncthreads();
   if (!s_role) return;
   __threadfence();
-  leaf_a_sums<XI>(p, slot, lb, stage);
+  if (CMC_LEAF_PAIRED && !XI)
+    leaf_a_sums_paired(p, slot, lb, stage);
+  else
+    leaf_a_sums<XI>(p, slot, lb, stage);
   if (p.fuse_tail) return;
   __threadfence();
   __syncthreads();
@@ -1395,7 +1465,7 @@ __global__ void __launch_bounds__(kGeneThreads, XI ? CMC_GENE_XI_MIN_BLOCKS : CM
   exp_table_init(exp_tab);
   __syncthreads();
   gene_sweep_body<JR, XI, PH>(p, m_off, smem, ExpTab(exp_tab));
-  // the lp buffer (at least 4 x 128 doubles, gene_sweep_smem_bytes) is free
+  // the lp buffer (at least 8 x 128 doubles, gene_sweep_smem_bytes) is free
   // now: it stages the leaf sums
   if constexpr (!XI && (PH & 2) != 0) {
     if (p.fuse_leaf_a) gene_leaf_epilogue<XI>(p, p.slot_base + blockIdx.y, *p.d_m + m_off, smem);
@@ -1765,7 +1835,7 @@ int gene_sweep_smem_bytes(int N, int Jmax) {
   // lp [N][B] and the group sums [2 Jmax][B]; at least kGeneThreads / 32
   // staging rows of kStage for the fused leaf sums
   const int rows = N + 2 * Jmax;
-  const int stage_rows = (kGeneThreads / 32) * kStage / kGeneThreads;
+  const int stage_rows = 2 * (kGeneThreads / 32) * kStage / kGeneThreads;  // paired leaf sums
   return (int)(sizeof(double) * (size_t)(rows > stage_rows ? rows : stage_rows) * kGeneThreads);
 }
 
