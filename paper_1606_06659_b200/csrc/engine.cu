@@ -2215,11 +2215,24 @@ int cmc_engine_trace(cmc_engine* e, long m_begin, long sweeps, unsigned long lon
   p.trace = d_tr;
   p.trace_n = d_n;
   p.trace_cap = (unsigned)cap;
-  CUDA_TRY(fork_lanes(e));
-  for (long off = 0; off < sweeps; ++off) CUDA_TRY(enqueue_all_lanes(e, p, off));
-  CUDA_TRY(join_lanes(e));
-  CUDA_TRY(launch_advance(e->d_m.p, sweeps, e->stream));
+  // the traced sweeps replay from one graph, as production sweeps do
+  // (eager launches add launch and cross-stream gaps of their own)
+  cudaGraph_t gr;
+  cudaGraphExec_t ge = nullptr;
+  CUDA_TRY(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t r = fork_lanes(e);
+  for (long off = 0; r == cudaSuccess && off < sweeps; ++off) r = enqueue_all_lanes(e, p, off);
+  if (r == cudaSuccess) r = join_lanes(e);
+  if (r == cudaSuccess) r = launch_advance(e->d_m.p, sweeps, e->stream);
+  cudaError_t r2 = cudaStreamEndCapture(e->stream, &gr);
+  CUDA_TRY(r);
+  CUDA_TRY(r2);
+  r = cudaGraphInstantiate(&ge, gr, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(gr);
+  CUDA_TRY(r);
+  CUDA_TRY(cudaGraphLaunch(ge, e->stream));
   CUDA_TRY(cudaStreamSynchronize(e->stream));
+  cudaGraphExecDestroy(ge);
   e->host_m = m_begin + sweeps;
   unsigned int n = 0;
   CUDA_TRY(cudaMemcpy(&n, d_n, sizeof(n), cudaMemcpyDeviceToHost));

@@ -166,6 +166,10 @@ __host__ __device__ inline int leaf_q_a(int L, int xi_any) { return 2 + L + (xi_
 __host__ __device__ inline int leaf_qs_a(int L, int xi_any) { return leaf_q_a(L, xi_any) + 1; }
 constexpr int kBlocksPerLeaf = kLeaf / kGeneThreads;  // gene blocks per reduction leaf
 constexpr int kStage = 128;  // values per warp per staging round of the serial leaf sums
+#ifndef CMC_STAGE_EPI
+#define CMC_STAGE_EPI 256
+#endif
+constexpr int kStageEpi = CMC_STAGE_EPI;  // the same in the gene kernel's epilogue (2 x per warp)
 
 // Launch wrappers (sweep_kernels.cu).  `chains` = grid.y.
 cudaError_t launch_eps_sweep(const SweepParams& p, int chains, long m_off,

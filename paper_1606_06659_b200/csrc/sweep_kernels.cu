@@ -738,7 +738,6 @@ using GeneRng = StreamSm;
 template <int JR, bool XI, int PH>
 __device__ __forceinline__ void gene_sweep_body(const SweepParams& p, const long m_off,
                                                 double* smem, const ExpTab etab) {
-  WarpTrace wt(p, 2, p.slot_base + blockIdx.y);
   __shared__ uint64_t rngq[4 * kGeneThreads];
   const unsigned rngq_s = (unsigned)__cvta_generic_to_shared(rngq + threadIdx.x);
   const int tid = threadIdx.x;
@@ -1200,6 +1199,50 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_PARK_MIN_BLOCKS)
 // one DADD per value with nothing else on it.  Padding past `end` with +0.0
 // is exact: the running sum starts at +0.0 and can never become -0.0, so
 // s + 0.0 == s.  Called by a whole warp; every lane gets the sum.
+// s + b[0] + b[1] + ... + b[n-1], left to right, from shared memory: the
+// loads of the next 16 values are issued before the 16 dependent additions
+// of the current ones, so the chain runs at the DADD latency instead of
+// load + add per value (timeline: 11.4 us per leaf epilogue warp before)
+// A/B (ms per sweep, 100-sweep calls, 4 chains / 1 chain): the pipelined
+// chain in the gene kernel's epilogue 0.3213 -> 0.3192 / 0.1295 -> 0.1274;
+// in the tail kernels' warp_serial_sum as well 0.3266 / 0.1257 -- a faster
+// high-priority tail takes SM time from the eps and gene kernels at 4
+// chains -- so the tail keeps the plain loop
+#ifndef CMC_TAIL_PIPE
+#define CMC_TAIL_PIPE 0
+#endif
+#ifndef CMC_EPI_PIPE
+#define CMC_EPI_PIPE 1
+#endif
+template <int B = 16>
+__device__ __forceinline__ double serial_add(const double* b, int n, double s) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  auto ld = [&](int i) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a + ((unsigned)i << 3)));
+    return v;
+  };
+  int i = 0;
+  if (n >= B) {
+    double t[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) t[j] = ld(j);
+    for (i = B; i + B <= n; i += B) {
+      double u[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) u[j] = ld(i + j);
+#pragma unroll
+      for (int j = 0; j < B; ++j) s += t[j];
+#pragma unroll
+      for (int j = 0; j < B; ++j) t[j] = u[j];
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) s += t[j];
+  }
+  for (; i < n; ++i) s += ld(i);
+  return s;
+}
+
 template <class V>
 __device__ __forceinline__ double warp_serial_sum(V value, long start, long end, double* buf) {
   const int lane = threadIdx.x & 31;
@@ -1224,8 +1267,12 @@ __device__ __forceinline__ double warp_serial_sum(V value, long start, long end,
       }
     }
     if (lane == 0) {
+#if CMC_TAIL_PIPE
+      s = serial_add(buf, kStage, s);
+#else
 #pragma unroll 16
       for (int i = 0; i < kStage; ++i) s += buf[i];
+#endif
     }
     __syncwarp();
   }
@@ -1342,6 +1389,9 @@ __device__ void leaf_a_sums(const SweepParams& p, int slot, long lb, double* sta
 #define CMC_LEAF_PAIRED 1
 #endif
 __device__ void leaf_a_sums_paired(const SweepParams& p, int slot, long lb, double* stage) {
+  // 256-value staging rounds (four per leaf), the next round's loads in
+  // flight while the current one is added
+  constexpr int kEpi = kStageEpi;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int L = p.L, Q = 2 + L, Qs = leaf_qs_a(L, 0);
   const size_t G = (size_t)p.G, so = (size_t)slot;
@@ -1349,14 +1399,14 @@ __device__ void leaf_a_sums_paired(const SweepParams& p, int slot, long lb, doub
   const long end = min((long)G, start + kLeaf);
   const long lpr = p.leaves_per_rank;
   const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
-  double* bufA = stage + (size_t)warp * 2 * kStage;
-  double* bufB = bufA + kStage;
+  double* bufA = stage + (size_t)warp * 2 * kEpi;
+  double* bufB = bufA + kEpi;
   auto src_of = [&](int q) -> const double* {
     return q < 2 ? (q == 0 ? p.log_gam : p.inv_gam) + so * G
                  : p.beta + so * L * G + (size_t)(q - 2) * G;
   };
-  constexpr int PER = kStage / 32;
-  const int chunks = (int)((end - start + kStage - 1) / kStage);
+  constexpr int PER = kEpi / 32;
+  const int chunks = (int)((end - start + kEpi - 1) / kEpi);
   for (int qa = warp; qa < Q; qa += 2 * nwarps) {
     const int qb = qa + nwarps;
     const double* A = src_of(qa);
@@ -1380,14 +1430,19 @@ __device__ void leaf_a_sums_paired(const SweepParams& p, int slot, long lb, doub
       if (c + 1 < chunks) {
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-          const long idx = start + (long)(c + 1) * kStage + k * 32 + lane;
+          const long idx = start + (long)(c + 1) * kEpi + k * 32 + lane;
           va[k] = idx < end ? __ldcg(A + idx) : 0.0;
           vb[k] = idx < end ? __ldcg(B + idx) : 0.0;
         }
       }
       if (lane < 2) {
+        const int n = (int)min((long)kEpi, end - start - (long)c * kEpi);
+#if CMC_EPI_PIPE
+        s = serial_add<8>(mine, n, s);
+#else
 #pragma unroll 16
-        for (int i = 0; i < kStage; ++i) s += mine[i];
+        for (int i = 0; i < n; ++i) s += mine[i];
+#endif
       }
       __syncwarp();
     }
@@ -1439,6 +1494,7 @@ __device__ void gene_leaf_epilogue(const SweepParams& p, int slot, long m, doubl
   }
   __syncthreads();
   if (!s_role) return;
+  WarpTrace wt(p, 6, slot);  // the leaf's serial sums (timeline only)
   __threadfence();
   if (CMC_LEAF_PAIRED && !XI)
     leaf_a_sums_paired(p, slot, lb, stage);
@@ -1464,8 +1520,9 @@ __global__ void __launch_bounds__(kGeneThreads, XI ? CMC_GENE_XI_MIN_BLOCKS : CM
   __shared__ double exp_tab[32];
   exp_table_init(exp_tab);
   __syncthreads();
+  WarpTrace wt(p, 2, p.slot_base + blockIdx.y);  // the body and the leaf epilogue
   gene_sweep_body<JR, XI, PH>(p, m_off, smem, ExpTab(exp_tab));
-  // the lp buffer (at least 8 x 128 doubles, gene_sweep_smem_bytes) is free
+  // the lp buffer (at least 16 x 128 doubles, gene_sweep_smem_bytes) is free
   // now: it stages the leaf sums
   if constexpr (!XI && (PH & 2) != 0) {
     if (p.fuse_leaf_a) gene_leaf_epilogue<XI>(p, p.slot_base + blockIdx.y, *p.d_m + m_off, smem);
@@ -1835,7 +1892,7 @@ int gene_sweep_smem_bytes(int N, int Jmax) {
   // lp [N][B] and the group sums [2 Jmax][B]; at least kGeneThreads / 32
   // staging rows of kStage for the fused leaf sums
   const int rows = N + 2 * Jmax;
-  const int stage_rows = 2 * (kGeneThreads / 32) * kStage / kGeneThreads;  // paired leaf sums
+  const int stage_rows = 2 * (kGeneThreads / 32) * kStageEpi / kGeneThreads;  // paired leaf sums
   return (int)(sizeof(double) * (size_t)(rows > stage_rows ? rows : stage_rows) * kGeneThreads);
 }
 

@@ -31,7 +31,7 @@ slot = ((r[:, 0] >> 48) & 0xff).astype(int)
 t0 = r[:, 1].min()
 st = (r[:, 1] - t0) / 1e3
 en = (r[:, 2] - t0) / 1e3
-names = {1: "eps", 2: "gene", 3: "leaf_a", 4: "leaf_b", 5: "hyper_a"}
+names = {1: "eps", 2: "gene", 3: "leaf_a", 4: "leaf_b", 5: "hyper_a", 6: "gene_epi"}
 lanes = 2 if C >= 2 else 1
 lane = slot * lanes // C
 rows = []
@@ -56,3 +56,9 @@ rows.sort()
 print(f"G={G} chains={C} lanes={lanes}: {S} sweeps, span {en.max():.1f} us ({en.max()/S:.1f} us/sweep)")
 for s_, e_, nm, ln, cnt in rows:
     print(f"  lane{ln} {nm:7s} {s_:9.1f} -> {e_:9.1f}  ({e_ - s_:7.1f} us, {cnt} warps)")
+
+m6 = kid == 6
+if m6.any():
+    d = en[m6] - st[m6]
+    print(f"gene-kernel leaf epilogues (last block of each leaf, per warp): {m6.sum()} warps, "
+          f"duration mean {d.mean():.1f} us, max {d.max():.1f} us")
