@@ -1211,6 +1211,9 @@ __global__ void __launch_bounds__(kGeneBlock, CMC_XI_PARK_MIN_BLOCKS)
 #ifndef CMC_TAIL_PIPE
 #define CMC_TAIL_PIPE 0
 #endif
+#ifndef CMC_TAIL_PIPE_B
+#define CMC_TAIL_PIPE_B 16
+#endif
 #ifndef CMC_EPI_PIPE
 #define CMC_EPI_PIPE 1
 #endif
@@ -1268,7 +1271,7 @@ __device__ __forceinline__ double warp_serial_sum(V value, long start, long end,
     }
     if (lane == 0) {
 #if CMC_TAIL_PIPE
-      s = serial_add(buf, kStage, s);
+      s = serial_add<CMC_TAIL_PIPE_B>(buf, kStage, s);
 #else
 #pragma unroll 16
       for (int i = 0; i < kStage; ++i) s += buf[i];
