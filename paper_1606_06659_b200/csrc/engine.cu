@@ -602,9 +602,11 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
     // build (100-sweep calls, two reps each, scripts/ab_e2e.sh): tail first
     // with gene = eps 0.3260, tail > eps > gene 0.3261, tail > gene > eps
     // 0.3224, tail = gene > eps 0.3214 ms; run() 1.981-1.988 s vs
-    // 1.991-1.998 s.
+    // 1.991-1.998 s.  Later: gene > tail > eps 0.3191 vs 0.3193 (level);
+    // gene first with the tail last 0.3540 (the tail must not wait).
+    // Modes 5 and 6 are those two.
 #ifndef CMC_PRIO_MODE
-#define CMC_PRIO_MODE 4  // A/B: 0 tail first, eps = gene; 1 all level; 2 tail > eps > gene; 3 tail > gene > eps; 4 tail = gene > eps
+#define CMC_PRIO_MODE 4  // A/B: 0 tail first, eps = gene; 1 all level; 2 tail > eps > gene; 3 tail > gene > eps; 4 tail = gene > eps; 5 gene > tail > eps; 6 gene > eps = tail
 #endif
     // With a t or Laplace prior (the plain xi kernel after the gene kernel,
     // at the gene kernel's priority) the gene kernel stays level with eps:
@@ -612,7 +614,7 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
     // xi kernel) follows the normal model: 0.6951 vs 0.7249 ms.
     bool hs = false;
     for (int v : e->prior) hs |= v == CMC_PRIOR_HORSESHOE;
-    const int mode = (CMC_PRIO_MODE == 4 && e->xi_any && !hs) ? 0 : CMC_PRIO_MODE;
+    const int mode = (CMC_PRIO_MODE >= 4 && e->xi_any && !hs) ? 0 : CMC_PRIO_MODE;
     const int mid = (least + greatest) / 2;
     p.prio_eps = least;
     p.prio_tail = mode == 1 ? least : greatest;
@@ -620,6 +622,8 @@ int ensure_device(cmc_engine* e, cmc_error* err) {
     if (mode == 2) p.prio_eps = mid;
     if (mode == 3) p.prio_gene = mid;
     if (mode == 4) p.prio_gene = greatest;
+    if (mode == 5) { p.prio_gene = greatest; p.prio_tail = mid; }
+    if (mode == 6) { p.prio_gene = greatest; p.prio_tail = least; }
   }
   CUDA_TRY(cudaStreamSynchronize(e->stream));
   e->dev_ready = true;
