@@ -1404,6 +1404,13 @@ __device__ void leaf_a_sums_paired(const SweepParams& p, int slot, long lb, doub
   const long rank = (p.g0 / kLeaf) / (lpr > 0 ? lpr : 1);
   double* bufA = stage + (size_t)warp * 2 * kEpi;
   double* bufB = bufA + kEpi;
+#ifdef CMC_DEBUG_BOUNDS
+  {  // the staging rounds fit the kernel's dynamic shared memory
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    assert((size_t)2 * nwarps * kEpi * sizeof(double) <= dyn);
+  }
+#endif
   auto src_of = [&](int q) -> const double* {
     return q < 2 ? (q == 0 ? p.log_gam : p.inv_gam) + so * G
                  : p.beta + so * L * G + (size_t)(q - 2) * G;
